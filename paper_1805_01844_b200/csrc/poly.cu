@@ -1,0 +1,422 @@
+// poly.cu -- host side of the C ABI declared in include/poly.h: argument
+// checks, regime selection, table upload, kernel launches.  One translation
+// unit (the device tables are module globals).
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "poly_common.cuh"
+#include "poly_compress.cuh"
+#include "poly_decompress.cuh"
+
+using namespace polyk;
+
+namespace {
+
+enum Regime { TILED = 0, LARGE = 1 };
+
+constexpr int MAX_DEVICES = 64;
+std::mutex g_mu;
+bool g_ready[MAX_DEVICES];
+int g_sms[MAX_DEVICES];
+
+typedef unsigned __int128 u128;
+
+// Host copies of the tables (exact integer arithmetic).
+uint8_t h_ktab[KTAB_MAX + 1];
+DecConst h_dtab[KTAB_MAX + 1];
+bool h_tables_built = false;
+
+void build_tables() {
+  if (h_tables_built) return;
+  const u128 word_ring = ((u128)1) << 64;
+  for (uint64_t B = 0; B <= KTAB_MAX; ++B) {
+    DecConst c;
+    memset(&c, 0, sizeof c);
+    uint32_t k = 0;
+    if (B >= 2) {
+      u128 p = 1;
+      while (p * B <= word_ring) {
+        p *= B;
+        ++k;
+      }
+      c.k = k;
+      if ((B & (B - 1)) == 0) {
+        uint32_t j = 0;
+        while ((1ull << j) != B) ++j;
+        c.log2b = j;
+      } else {
+        const uint64_t D = (uint64_t)p;  // B^k < 2^64 for non-powers of two
+        u128 rem = 0, q = 0;
+        for (int i = 160; i >= 0; --i) {
+          rem = (rem << 1) | (i == 160 ? 1u : 0u);
+          q <<= 1;
+          if (rem >= D) {
+            rem -= D;
+            q |= 1;
+          }
+        }
+        q += 1;  // ceil: the remainder of 2^160 / D is nonzero
+        c.Bk = D;
+        c.Rl = (uint64_t)q;
+        c.Rh = (uint64_t)(q >> 64);
+      }
+    }
+    h_ktab[B] = (uint8_t)k;
+    h_dtab[B] = c;
+  }
+  h_tables_built = true;
+}
+
+template <typename K>
+void set_smem_attr(K kernel, int bytes) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+uint32_t tiled_smem_compress(uint32_t T) { return TILE_BYTES + 8 * MAX_WORDS + 16 * T; }
+uint32_t tiled_smem_decompress(uint32_t T) { return TILE_BYTES + 8 * MAX_WORDS + 60 * T; }
+template <typename V>
+uint32_t large_smem_pack() { return ((CH_VALUES + 64) * sizeof(V) + 15) / 16 * 16; }
+template <typename V>
+uint32_t large_smem_unpack() {
+  return 16 * ((CH_VALUES + 64) * sizeof(V) / 16 + 1) + 8 * (CH_VALUES / 2 + 2);
+}
+
+poly_status_t ensure_init(int dev) {
+  if (dev < 0 || dev >= MAX_DEVICES) return POLY_ERR_INVALID_ARG;
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_ready[dev]) return POLY_OK;
+  build_tables();
+  int cur = 0;
+  if (cudaGetDevice(&cur) != cudaSuccess) return POLY_ERR_CUDA;
+  if (cur != dev && cudaSetDevice(dev) != cudaSuccess) return POLY_ERR_CUDA;
+  cudaError_t e = cudaMemcpyToSymbol(g_ktab, h_ktab, sizeof h_ktab);
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_dtab, h_dtab, sizeof h_dtab);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
+  const int tc = tiled_smem_compress(T_MAX), td = tiled_smem_decompress(T_MAX);
+  set_smem_attr(poly_compress_tiled<uint16_t>, tc);
+  set_smem_attr(poly_compress_tiled<uint32_t>, tc);
+  set_smem_attr(poly_decompress_tiled<uint16_t>, td);
+  set_smem_attr(poly_decompress_tiled<uint32_t>, td);
+  set_smem_attr(poly_compress_pack<uint16_t>, large_smem_pack<uint16_t>());
+  set_smem_attr(poly_compress_pack<uint32_t>, large_smem_pack<uint32_t>());
+  set_smem_attr(poly_decompress_unpack<uint16_t>, large_smem_unpack<uint16_t>());
+  set_smem_attr(poly_decompress_unpack<uint32_t>, large_smem_unpack<uint32_t>());
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (cur != dev) cudaSetDevice(cur);
+  if (e != cudaSuccess) return POLY_ERR_CUDA;
+  g_ready[dev] = true;
+  return POLY_OK;
+}
+
+uint32_t gcd32(uint32_t a, uint32_t b) {
+  while (b) {
+    uint32_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+// Regime and launch shape for (n, w, block_size).  Deterministic: the same
+// arguments always give the same shape (the stream does not depend on it).
+bool plan(uint64_t n, uint32_t w, uint64_t block_size, Shape& sh, Regime& rg) {
+  if (n == 0 || (w != 16 && w != 32) || block_size >= (1ull << 32)) return false;
+  memset(&sh, 0, sizeof sh);
+  sh.n = n;
+  sh.width = w;
+  sh.block_len = (uint32_t)block_size;
+  sh.Le = block_size == 0 ? n : block_size;
+  sh.n_blocks = (n + sh.Le - 1) / sh.Le;
+  if (sh.n_blocks >= (1ull << 32)) return false;
+  const uint32_t vb = w / 8;
+  const uint64_t TV = TILE_BYTES / vb;
+  if (sh.Le <= TV) {
+    rg = TILED;
+    const uint64_t kmin = w == 16 ? 4 : 2;
+    uint64_t T = TV / sh.Le;
+    T = std::min<uint64_t>(T, T_MAX);
+    T = std::min<uint64_t>(T, MAX_WORDS / ((sh.Le + kmin - 1) / kmin));
+    if (T >= (uint64_t)NT) {
+      T = T / NT * NT;
+    } else {
+      const uint64_t ta = 16 / gcd32(16, (uint32_t)((sh.Le * vb) % 16 ? (sh.Le * vb) % 16 : 16));
+      if (T >= ta) T = T / ta * ta;
+    }
+    if (T < 1) T = 1;
+    sh.T = (uint32_t)T;
+    uint32_t G = 1;
+    if (T < (uint64_t)NT) {
+      const uint32_t q = (uint32_t)(NT / T);
+      while (G * 2 <= q) G *= 2;
+    }
+    sh.G = G;
+    sh.n_tiles = (sh.n_blocks + T - 1) / T;
+  } else {
+    rg = LARGE;
+    sh.cpb = (sh.Le + CH_VALUES - 1) / CH_VALUES;
+    sh.n_chunks = sh.n_blocks * sh.cpb;
+    sh.n_stiles = (sh.n_blocks + SCAN_T - 1) / SCAN_T;
+  }
+  return true;
+}
+
+struct WsLayout {
+  uint64_t status_off, bmin_off, bmax_off, woff_off, total;
+};
+
+WsLayout ws_layout(const Shape& sh, Regime rg) {
+  WsLayout L;
+  memset(&L, 0, sizeof L);
+  L.status_off = 64;
+  if (rg == TILED) {
+    L.total = 64 + 8 * sh.n_tiles;
+  } else {
+    L.bmin_off = (64 + 8 * sh.n_stiles + 15) / 16 * 16;
+    L.bmax_off = (L.bmin_off + 4 * sh.n_blocks + 15) / 16 * 16;
+    L.woff_off = (L.bmax_off + 4 * sh.n_blocks + 15) / 16 * 16;
+    L.total = L.woff_off + 8 * sh.n_blocks;
+  }
+  return L;
+}
+
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+int grid_for(uint64_t work, int dev) {
+  const uint64_t cap = (uint64_t)(g_sms[dev] > 0 ? g_sms[dev] : 148) * 8;
+  return (int)std::min<uint64_t>(work, cap);
+}
+
+}  // namespace
+
+extern "C" {
+
+int poly_version(void) { return 100; }
+
+const char* poly_status_string(poly_status_t s) {
+  switch (s) {
+    case POLY_OK: return "POLY_OK";
+    case POLY_ERR_INVALID_ARG: return "POLY_ERR_INVALID_ARG";
+    case POLY_ERR_EMPTY_INPUT: return "POLY_ERR_EMPTY_INPUT";
+    case POLY_ERR_CAPACITY: return "POLY_ERR_CAPACITY";
+    case POLY_ERR_WORKSPACE: return "POLY_ERR_WORKSPACE";
+    case POLY_ERR_CUDA: return "POLY_ERR_CUDA";
+    case POLY_ERR_CORRUPT: return "POLY_ERR_CORRUPT";
+  }
+  return "POLY_UNKNOWN";
+}
+
+poly_status_t poly_init(int device) { return ensure_init(device); }
+
+uint64_t poly_max_compressed_bytes(uint64_t n, poly_dtype_t dt, uint64_t block_size) {
+  if (n == 0 || (dt != POLY_U16 && dt != POLY_U32)) return 0;
+  const uint64_t L = block_size == 0 ? n : block_size;
+  const uint64_t nb = (n + L - 1) / L;
+  const uint64_t kmin = dt == POLY_U16 ? 4 : 2;
+  const uint64_t full = n / L, last = n - full * L;
+  uint64_t words = full * ((L + kmin - 1) / kmin);
+  if (last) words += (last + kmin - 1) / kmin;
+  return 32 + 16 * nb + 8 * words;
+}
+
+uint64_t poly_workspace_bytes(uint64_t n, poly_dtype_t dt, uint64_t block_size) {
+  Shape sh;
+  Regime rg;
+  if (!plan(n, (uint32_t)dt, block_size, sh, rg)) return 0;
+  return ws_layout(sh, rg).total;
+}
+
+int poly_launches_per_call(uint64_t n, poly_dtype_t dt, uint64_t block_size, int decompress) {
+  Shape sh;
+  Regime rg;
+  if (!plan(n, (uint32_t)dt, block_size, sh, rg)) return 0;
+  if (rg == TILED) return 1;
+  return decompress ? 2 : 3;
+}
+
+poly_status_t poly_compress(const void* d_in, uint64_t n, poly_dtype_t dt, uint64_t block_size,
+                            void* d_out, uint64_t out_capacity, uint64_t* d_compressed_bytes,
+                            void* d_workspace, uint64_t workspace_bytes, void* stream) {
+  if (dt != POLY_U16 && dt != POLY_U32) return POLY_ERR_INVALID_ARG;
+  if (n == 0) return POLY_ERR_EMPTY_INPUT;
+  if (!d_in || !d_out || !d_compressed_bytes || !d_workspace) return POLY_ERR_INVALID_ARG;
+  const uint32_t vb = (uint32_t)dt / 8;
+  if ((reinterpret_cast<uintptr_t>(d_in) % vb) != 0) return POLY_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(d_out) & 15) != 0) return POLY_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(d_compressed_bytes) & 7) != 0) return POLY_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(d_workspace) & 15) != 0) return POLY_ERR_INVALID_ARG;
+  Shape sh;
+  Regime rg;
+  if (!plan(n, (uint32_t)dt, block_size, sh, rg)) return POLY_ERR_INVALID_ARG;
+  if (out_capacity < poly_max_compressed_bytes(n, dt, block_size)) return POLY_ERR_CAPACITY;
+  const WsLayout W = ws_layout(sh, rg);
+  if (workspace_bytes < W.total) return POLY_ERR_WORKSPACE;
+  const int dev = current_device();
+  poly_status_t st = ensure_init(dev);
+  if (st != POLY_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(d_workspace);
+
+  CompressArgs a;
+  memset(&a, 0, sizeof a);
+  a.in = d_in;
+  a.out = reinterpret_cast<uint8_t*>(d_out);
+  a.compressed_bytes = d_compressed_bytes;
+  a.ticket = reinterpret_cast<uint32_t*>(ws);
+  a.status = reinterpret_cast<uint64_t*>(ws + W.status_off);
+  a.sh = sh;
+  if (rg == TILED) {
+    cudaMemsetAsync(ws, 0, W.total, s);
+    const uint32_t smem = tiled_smem_compress(sh.T);
+    if (dt == POLY_U16)
+      poly_compress_tiled<uint16_t><<<(unsigned)sh.n_tiles, NT, smem, s>>>(a);
+    else
+      poly_compress_tiled<uint32_t><<<(unsigned)sh.n_tiles, NT, smem, s>>>(a);
+  } else {
+    a.bmin = reinterpret_cast<uint32_t*>(ws + W.bmin_off);
+    a.bmax = reinterpret_cast<uint32_t*>(ws + W.bmax_off);
+    a.woff = reinterpret_cast<uint64_t*>(ws + W.woff_off);
+    cudaMemsetAsync(ws, 0, W.bmin_off, s);
+    cudaMemsetAsync(a.bmin, 0xff, 4 * sh.n_blocks, s);
+    cudaMemsetAsync(a.bmax, 0, 4 * sh.n_blocks, s);
+    const int gr = grid_for(sh.n_chunks, dev);
+    if (dt == POLY_U16) {
+      poly_compress_minmax<uint16_t><<<gr, NT, 0, s>>>(a);
+      poly_compress_block_scan<<<(unsigned)sh.n_stiles, NT, 0, s>>>(a);
+      poly_compress_pack<uint16_t><<<gr, NT, large_smem_pack<uint16_t>(), s>>>(a);
+    } else {
+      poly_compress_minmax<uint32_t><<<gr, NT, 0, s>>>(a);
+      poly_compress_block_scan<<<(unsigned)sh.n_stiles, NT, 0, s>>>(a);
+      poly_compress_pack<uint32_t><<<gr, NT, large_smem_pack<uint32_t>(), s>>>(a);
+    }
+  }
+  if (cudaGetLastError() != cudaSuccess) return POLY_ERR_CUDA;
+  return POLY_OK;
+}
+
+poly_status_t poly_read_header(const void* h_hdr32, uint64_t* n, poly_dtype_t* dt,
+                               uint64_t* block_size, uint64_t* n_blocks, uint64_t* payload_bytes) {
+  if (!h_hdr32) return POLY_ERR_INVALID_ARG;
+  const uint8_t* p = reinterpret_cast<const uint8_t*>(h_hdr32);
+  if (memcmp(p, "PLYC", 4) != 0 || p[4] != 2 || p[5] != 0 || p[7] != 0 || (p[6] != 16 && p[6] != 32))
+    return POLY_ERR_CORRUPT;
+  uint64_t nn, pb;
+  uint32_t bl, nb;
+  memcpy(&nn, p + 8, 8);
+  memcpy(&bl, p + 16, 4);
+  memcpy(&nb, p + 20, 4);
+  memcpy(&pb, p + 24, 8);
+  if (n) *n = nn;
+  if (dt) *dt = (poly_dtype_t)p[6];
+  if (block_size) *block_size = bl;
+  if (n_blocks) *n_blocks = nb;
+  if (payload_bytes) *payload_bytes = pb;
+  return POLY_OK;
+}
+
+poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_dtype_t dt,
+                              uint64_t n, uint64_t block_size, void* d_out, uint32_t* d_status,
+                              void* d_workspace, uint64_t workspace_bytes, void* stream) {
+  if (dt != POLY_U16 && dt != POLY_U32) return POLY_ERR_INVALID_ARG;
+  if (n == 0) return POLY_ERR_EMPTY_INPUT;
+  if (!d_in || !d_out || !d_status || !d_workspace) return POLY_ERR_INVALID_ARG;
+  const uint32_t vb = (uint32_t)dt / 8;
+  if ((reinterpret_cast<uintptr_t>(d_in) & 15) != 0) return POLY_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(d_out) % vb) != 0) return POLY_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(d_workspace) & 15) != 0) return POLY_ERR_INVALID_ARG;
+  Shape sh;
+  Regime rg;
+  if (!plan(n, (uint32_t)dt, block_size, sh, rg)) return POLY_ERR_INVALID_ARG;
+  const WsLayout W = ws_layout(sh, rg);
+  if (workspace_bytes < W.total) return POLY_ERR_WORKSPACE;
+  const int dev = current_device();
+  poly_status_t st = ensure_init(dev);
+  if (st != POLY_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(d_workspace);
+
+  DecompressArgs a;
+  memset(&a, 0, sizeof a);
+  a.in = reinterpret_cast<const uint8_t*>(d_in);
+  a.compressed_bytes = compressed_bytes;
+  a.out = d_out;
+  a.status_out = d_status;
+  a.ticket = reinterpret_cast<uint32_t*>(ws);
+  a.status = reinterpret_cast<uint64_t*>(ws + W.status_off);
+  a.sh = sh;
+  cudaMemsetAsync(d_status, 0, 4, s);
+  if (rg == TILED) {
+    cudaMemsetAsync(ws, 0, W.total, s);
+    const uint32_t smem = tiled_smem_decompress(sh.T);
+    if (dt == POLY_U16)
+      poly_decompress_tiled<uint16_t><<<(unsigned)sh.n_tiles, NT, smem, s>>>(a);
+    else
+      poly_decompress_tiled<uint32_t><<<(unsigned)sh.n_tiles, NT, smem, s>>>(a);
+  } else {
+    a.woff = reinterpret_cast<uint64_t*>(ws + W.woff_off);
+    cudaMemsetAsync(ws, 0, W.bmin_off, s);
+    const int gr = grid_for(sh.n_chunks, dev);
+    poly_decompress_block_scan<<<(unsigned)sh.n_stiles, NT, 0, s>>>(a);
+    if (dt == POLY_U16)
+      poly_decompress_unpack<uint16_t><<<gr, NT, large_smem_unpack<uint16_t>(), s>>>(a);
+    else
+      poly_decompress_unpack<uint32_t><<<gr, NT, large_smem_unpack<uint32_t>(), s>>>(a);
+  }
+  if (cudaGetLastError() != cudaSuccess) return POLY_ERR_CUDA;
+  return POLY_OK;
+}
+
+poly_status_t poly_compress_host(const void* h_in, uint64_t n, poly_dtype_t dt, uint64_t block_size,
+                                 void* h_out, uint64_t h_out_capacity, uint64_t* h_compressed_bytes,
+                                 void* d_in_scratch, void* d_out_scratch, uint64_t d_out_capacity,
+                                 void* d_workspace, uint64_t workspace_bytes, void* stream) {
+  if (!h_in || !h_out || !h_compressed_bytes || !d_in_scratch) return POLY_ERR_INVALID_ARG;
+  if (dt != POLY_U16 && dt != POLY_U32) return POLY_ERR_INVALID_ARG;
+  if (n == 0) return POLY_ERR_EMPTY_INPUT;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(d_workspace);
+  if (!ws) return POLY_ERR_INVALID_ARG;
+  if (cudaMemcpyAsync(d_in_scratch, h_in, n * ((uint32_t)dt / 8), cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return POLY_ERR_CUDA;
+  uint64_t* d_nbytes = reinterpret_cast<uint64_t*>(ws + 8);
+  poly_status_t st = poly_compress(d_in_scratch, n, dt, block_size, d_out_scratch, d_out_capacity,
+                                   d_nbytes, d_workspace, workspace_bytes, stream);
+  if (st != POLY_OK) return st;
+  if (cudaMemcpyAsync(h_compressed_bytes, d_nbytes, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return POLY_ERR_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return POLY_ERR_CUDA;
+  if (*h_compressed_bytes > h_out_capacity) return POLY_ERR_CAPACITY;
+  if (cudaMemcpyAsync(h_out, d_out_scratch, *h_compressed_bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return POLY_ERR_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return POLY_ERR_CUDA;
+  return POLY_OK;
+}
+
+poly_status_t poly_decompress_host(const void* h_in, uint64_t compressed_bytes, poly_dtype_t dt,
+                                   uint64_t n, uint64_t block_size, void* h_out, uint32_t* h_status,
+                                   void* d_in_scratch, void* d_out_scratch,
+                                   void* d_workspace, uint64_t workspace_bytes, void* stream) {
+  if (!h_in || !h_out || !h_status || !d_in_scratch || !d_out_scratch || !d_workspace)
+    return POLY_ERR_INVALID_ARG;
+  if (dt != POLY_U16 && dt != POLY_U32) return POLY_ERR_INVALID_ARG;
+  if (n == 0) return POLY_ERR_EMPTY_INPUT;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(d_workspace);
+  if (cudaMemcpyAsync(d_in_scratch, h_in, compressed_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return POLY_ERR_CUDA;
+  uint32_t* d_st = reinterpret_cast<uint32_t*>(ws + 16);
+  poly_status_t st = poly_decompress(d_in_scratch, compressed_bytes, dt, n, block_size, d_out_scratch,
+                                     d_st, d_workspace, workspace_bytes, stream);
+  if (st != POLY_OK) return st;
+  if (cudaMemcpyAsync(h_out, d_out_scratch, n * ((uint32_t)dt / 8), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return POLY_ERR_CUDA;
+  if (cudaMemcpyAsync(h_status, d_st, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return POLY_ERR_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return POLY_ERR_CUDA;
+  return POLY_OK;
+}
+
+}  // extern "C"

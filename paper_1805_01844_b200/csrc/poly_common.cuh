@@ -1,0 +1,250 @@
+// poly_common.cuh -- shared device pieces of the sm_100a polynomial codec:
+// launch constants, the B -> k / reciprocal tables,
+// global-memory access helpers and the single-pass decoupled look-back scan
+// (a4).  Nothing here is shared with oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/poly.h"
+
+namespace polyk {
+
+constexpr int NT = 256;                 // threads per CTA (8 warps)
+constexpr int NWARP = NT / 32;
+constexpr uint32_t TILE_BYTES = 16384;  // input bytes staged per tiled CTA
+constexpr uint32_t MAX_WORDS = 2560;    // payload words staged per tile (20 KiB)
+constexpr uint32_t T_MAX = 512;         // blocks per tile
+constexpr uint32_t CH_VALUES = 8192;    // values per chunk in the large-block regime
+constexpr uint32_t KTAB_MAX = 65536;    // B <= KTAB_MAX use the tables
+
+// look-back status word: [63:62] flag, [61:0] value
+constexpr uint64_t FLAG_AGG = 1ull << 62;
+constexpr uint64_t FLAG_PRE = 2ull << 62;
+constexpr uint64_t VAL_MASK = (1ull << 62) - 1;
+
+constexpr uint32_t CODEC_CONSTANT = 1;
+constexpr uint32_t CODEC_BASIC = 2;
+
+// Per-base decode constants.  For a non-power-of-two
+// base B with capacity k:  Bk = B^k < 2^64 and R = ceil(2^160 / B^k) < 2^128,
+// split R = Rh * 2^64 + Rl.  For B = 2^j the decoder uses shifts instead and
+// only k is meaningful.
+struct __align__(16) DecConst {
+  uint64_t Bk;
+  uint64_t Rl;
+  uint64_t Rh;
+  uint32_t k;
+  uint32_t log2b;  // j if B = 2^j, else 0
+};
+
+// Filled once per device by poly_init (host computes them with exact 128-bit
+// integer arithmetic).
+__device__ uint8_t g_ktab[KTAB_MAX + 1];
+__device__ DecConst g_dtab[KTAB_MAX + 1];
+
+// ---------------------------------------------------------------- arithmetic
+// Exact k = max{k : B^k <= 2^64} for B > KTAB_MAX: B^3 <= 2^64 iff B <= 2642245.
+__device__ __forceinline__ uint32_t capacity_of(uint64_t B) {
+  if (B <= KTAB_MAX) return g_ktab[B];
+  return B <= 2642245ull ? 3u : 2u;
+}
+
+// ceil(2^160 / D) for D not a power of two, D >= 3 (slow path for B > 2^16):
+// restoring long division, 161 quotient bits, result < 2^128.
+__device__ __noinline__ void recip160(uint64_t D, uint64_t& Rl, uint64_t& Rh) {
+  unsigned __int128 rem = 0, q = 0;
+  for (int i = 160; i >= 0; --i) {
+    rem = (rem << 1) | (i == 160 ? 1u : 0u);
+    q <<= 1;
+    if (rem >= D) {
+      rem -= D;
+      q |= 1;
+    }
+  }
+  q += 1;  // D is not a power of two, so the remainder is nonzero: ceil = floor + 1
+  Rl = (uint64_t)q;
+  Rh = (uint64_t)(q >> 64);
+}
+
+__device__ __forceinline__ DecConst dec_const_of(uint64_t B) {
+  if (B <= KTAB_MAX) return g_dtab[B];
+  DecConst c;
+  c.k = capacity_of(B);
+  c.log2b = ((B & (B - 1)) == 0) ? (uint32_t)(63 - __clzll(B)) : 0u;
+  if (c.log2b) {
+    c.Bk = 0; c.Rl = 0; c.Rh = 0;
+  } else {
+    uint64_t p = 1;
+    for (uint32_t i = 0; i < c.k; ++i) p *= B;
+    c.Bk = p;
+    recip160(p, c.Rl, c.Rh);
+  }
+  return c;
+}
+
+// ---------------------------------------------------------------- memory
+__device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ uint64_t ldg_nc_u64(const void* p) {
+  uint64_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(r) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void stg_cs_v4(void* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ---------------------------------------------------------------- warp/CTA
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Exclusive scan of in[0..count) into out[0..count) over the CTA; returns the
+// total.  Every thread must call it.  s_warp: NWARP entries of scratch.
+template <typename T>
+__device__ T cta_exclusive_scan(const T* in, T* out, uint32_t count, T* s_warp) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t q = (count + NT - 1) / NT;
+  const uint32_t i0 = min((uint32_t)tid * q, count), i1 = min(i0 + q, count);
+  T local = 0;
+  for (uint32_t i = i0; i < i1; ++i) local += in[i];
+  T x = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    T w = lane < NWARP ? s_warp[lane] : (T)0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      T y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < NWARP) s_warp[lane] = w;
+  }
+  __syncthreads();
+  T excl = x - local + (warp > 0 ? s_warp[warp - 1] : (T)0);
+  const T total = s_warp[NWARP - 1];
+  for (uint32_t i = i0; i < i1; ++i) {
+    T v = in[i];
+    out[i] = excl;
+    excl += v;
+  }
+  __syncthreads();
+  return total;
+}
+
+// Decoupled look-back (single-pass scan): called by all 32 lanes of one warp
+// for `tile` >= 1 after the tile published its aggregate; returns the
+// exclusive prefix of the tile (same value in every lane).  Tiles are handed
+// out in order by an atomic ticket, so every predecessor is resident or done
+// and the spin terminates.
+__device__ __forceinline__ uint64_t lookback(const uint64_t* status, uint64_t tile) {
+  const int lane = threadIdx.x & 31;
+  uint64_t excl = 0;
+  int64_t base = (int64_t)tile - 1;
+  while (true) {
+    const int64_t idx = base - lane;
+    uint64_t st = FLAG_PRE;  // before tile 0: prefix 0
+    if (idx >= 0) {
+      do {
+        st = ld_relaxed_u64(status + idx);
+      } while ((st >> 62) == 0);
+    }
+    const uint32_t pre = __ballot_sync(0xffffffffu, (st & FLAG_PRE) != 0);
+    uint64_t v = st & VAL_MASK;
+    if (pre) {
+      const int first = __ffs(pre) - 1;
+      if (lane > first) v = 0;
+      return excl + warp_sum_u64(v);
+    }
+    excl += warp_sum_u64(v);
+    base -= 32;
+  }
+}
+
+__device__ __forceinline__ uint32_t shfl_min(uint32_t v, int w) {
+  for (int o = w >> 1; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ uint32_t shfl_max(uint32_t v, int w) {
+  for (int o = w >> 1; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Copy nv values of type V from global g to shared s (16-byte vector loads
+// when g is 16-byte aligned, scalar otherwise and for the tail).
+template <typename V>
+__device__ __forceinline__ void load_values(V* s, const V* g, uint32_t nv) {
+  const int tid = threadIdx.x;
+  const uint32_t nbytes = nv * (uint32_t)sizeof(V);
+  uint32_t done = 0;
+  if ((reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+    const uint32_t n16 = nbytes >> 4;
+    const uint8_t* gb = reinterpret_cast<const uint8_t*>(g);
+    uint4* sb = reinterpret_cast<uint4*>(s);
+#pragma unroll 4
+    for (uint32_t i = tid; i < n16; i += NT) sb[i] = ldg_nc_v4(gb + 16ull * i);
+    done = (n16 << 4) / (uint32_t)sizeof(V);
+  }
+  for (uint32_t i = done + tid; i < nv; i += NT) s[i] = g[i];
+}
+
+// Copy nv values from shared s to global g (16-byte stores when aligned).
+template <typename V>
+__device__ __forceinline__ void store_values(V* g, const V* s, uint32_t nv) {
+  const int tid = threadIdx.x;
+  uint32_t done = 0;
+  if ((reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+    const uint32_t n16 = (nv * (uint32_t)sizeof(V)) >> 4;
+    uint8_t* gb = reinterpret_cast<uint8_t*>(g);
+    const uint4* sb = reinterpret_cast<const uint4*>(s);
+#pragma unroll 4
+    for (uint32_t i = tid; i < n16; i += NT) stg_cs_v4(gb + 16ull * i, sb[i]);
+    done = (n16 << 4) / (uint32_t)sizeof(V);
+  }
+  for (uint32_t i = done + tid; i < nv; i += NT) g[i] = s[i];
+}
+
+// Launch-time description of one call (identical for the compress and the
+// decompress side; see poly_api.cu plan()).
+struct Shape {
+  uint64_t n;
+  uint64_t Le;          // effective block length
+  uint64_t n_blocks;
+  uint32_t block_len;   // as given (0 = whole), stored in the global header
+  uint32_t width;       // 16 or 32
+  uint32_t T;           // blocks per tile (tiled regime)
+  uint32_t G;           // threads per block group (tiled regime), power of two
+  uint64_t n_tiles;     // tiled regime
+  uint64_t cpb;         // chunks per block (large regime)
+  uint64_t n_chunks;    // large regime
+  uint64_t n_stiles;    // scan tiles over blocks (large regime)
+};
+
+}  // namespace polyk

@@ -1,0 +1,100 @@
+"""The C-ABI library loads without a GPU and exports every symbol include/poly.h
+declares; host-only entry points (sizes, header parse, argument checks) work
+on the CPU.  No compute call is made here."""
+import ctypes
+import os
+import re
+import struct
+
+import pytest
+
+from paper_1805_01844_b200 import _build, polycomp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    _build.build()
+    return polycomp.load_library()
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "poly.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(poly_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_every_declared_symbol_is_exported(lib):
+    names = declared_functions()
+    assert len(names) >= 10
+    for name in names:
+        assert hasattr(lib, name), name
+    assert sorted(polycomp.EXPORTS) == names
+
+
+def test_version_and_status_strings(lib):
+    assert polycomp.poly_version() >= 100
+    assert lib.poly_status_string(0) == b"POLY_OK"
+    assert lib.poly_status_string(2) == b"POLY_ERR_EMPTY_INPUT"
+
+
+def test_max_compressed_bytes_closed_form(lib):
+    # 32 + 16*n_blocks + 8*sum ceil(n_b / k_min); k_min = 4 (u16), 2 (u32)
+    def bound(n, w, L):
+        Le = n if L == 0 else L
+        kmin = 4 if w == 16 else 2
+        sizes = [min(Le, n - lo) for lo in range(0, n, Le)]
+        return 32 + 16 * len(sizes) + 8 * sum(-(-s // kmin) for s in sizes)
+    for n, w, L in [(1, 16, 0), (7, 16, 3), (1000, 32, 7), (1 << 20, 16, 0), (556500, 16, 30), (12345, 32, 1)]:
+        assert polycomp.poly_max_compressed_bytes(n, w, L) == bound(n, w, L)
+    assert polycomp.poly_max_compressed_bytes(0, 16, 0) == 0
+
+
+def test_workspace_bytes_positive(lib):
+    for n, w, L in [(1, 16, 0), (556500000, 16, 30), (1 << 28, 32, 65536), (1 << 31, 16, 4096), (1 << 20, 16, 0)]:
+        assert polycomp.poly_workspace_bytes(n, w, L) >= 64
+    assert polycomp.poly_workspace_bytes(0, 16, 0) == 0
+    assert polycomp.poly_workspace_bytes(10, 8, 0) == 0
+
+
+def test_launches_per_call(lib):
+    assert polycomp.poly_launches_per_call(556500000, 16, 30, False) == 1
+    assert polycomp.poly_launches_per_call(1 << 20, 16, 0, False) == 3
+    assert polycomp.poly_launches_per_call(1 << 20, 16, 0, True) == 2
+
+
+def test_argument_errors_without_launch(lib):
+    vp = ctypes.c_void_p
+    # n == 0 -> EMPTY_INPUT before anything touches CUDA
+    assert lib.poly_compress(vp(16), 0, 16, 0, vp(16), 1 << 20, vp(16), vp(16), 1 << 20, None) == 2
+    # bad dtype, null pointers, block_size >= 2^32
+    assert lib.poly_compress(vp(16), 10, 8, 0, vp(16), 1 << 20, vp(16), vp(16), 1 << 20, None) == 1
+    assert lib.poly_compress(None, 10, 16, 0, vp(16), 1 << 20, vp(16), vp(16), 1 << 20, None) == 1
+    assert lib.poly_compress(vp(16), 10, 16, 1 << 32, vp(16), 1 << 20, vp(16), vp(16), 1 << 20, None) == 1
+    # misaligned output buffer
+    assert lib.poly_compress(vp(16), 10, 16, 0, vp(17), 1 << 20, vp(16), vp(16), 1 << 20, None) == 1
+    # capacity / workspace too small
+    assert lib.poly_compress(vp(16), 1000, 16, 0, vp(16), 10, vp(16), vp(16), 1 << 20, None) == 3
+    assert lib.poly_compress(vp(16), 1 << 20, 16, 30, vp(16), 1 << 24, vp(16), vp(16), 8, None) == 4
+    assert lib.poly_decompress(vp(16), 100, 16, 0, 0, vp(16), vp(16), vp(16), 1 << 20, None) == 2
+    assert lib.poly_decompress(vp(16), 100, 16, 10, 0, vp(16), vp(16), vp(16), 8, None) == 4
+
+
+def test_read_header(lib):
+    hdr = b"PLYC" + bytes([2, 0, 16, 0]) + struct.pack("<QIIQ", 7, 3, 3, 8)
+    assert polycomp.poly_read_header(hdr) == {"n": 7, "dtype": 16, "block_len": 3, "n_blocks": 3,
+                                              "payload_bytes": 8}
+    with pytest.raises(polycomp.PolyError):
+        polycomp.poly_read_header(b"XXXX" + hdr[4:])
+    with pytest.raises(polycomp.PolyError):
+        polycomp.poly_read_header(hdr[:4] + b"\x01" + hdr[5:])
+
+
+def test_product_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_1805_01844_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*|//.*", "", src).replace("oracle/", ""), f

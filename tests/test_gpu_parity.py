@@ -1,0 +1,199 @@
+"""GPU parity: the CUDA path through the C ABI against the C oracle, bit for
+bit (compressed stream) and value for value (decompressed array), on seeded
+inputs.  Marked gpu: run on a B200 with `pytest -m gpu`."""
+import struct
+
+import numpy as np
+import pytest
+import torch
+
+import workloads
+from paper_1805_01844_b200 import polycomp as pc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    pc.poly_init()
+
+
+def to_dev(x: np.ndarray) -> torch.Tensor:
+    t = torch.from_numpy(x.view(np.int16 if x.dtype == np.uint16 else np.int32).copy())
+    return t.view(torch.uint16 if x.dtype == np.uint16 else torch.uint32).cuda()
+
+
+def gpu_roundtrip(x_dev: torch.Tensor, L: int):
+    out, nb = pc.poly_compress(x_dev, L)
+    nbytes = int(nb.item())
+    stream = out[:nbytes]
+    dt = 16 if x_dev.dtype == torch.uint16 else 32
+    y, st = pc.poly_decompress(out, nbytes, dt, x_dev.numel(), L)
+    torch.cuda.synchronize()
+    return stream.cpu().numpy().tobytes(), y, int(st.item())
+
+
+def check_case(oracle_lib, x: np.ndarray, L: int):
+    x_dev = to_dev(x)
+    s_gpu, y, st = gpu_roundtrip(x_dev, L)
+    s_ref = oracle_lib.compress(x, L)
+    assert len(s_gpu) == len(s_ref), (len(s_gpu), len(s_ref))
+    if s_gpu != s_ref:
+        a = np.frombuffer(s_gpu, np.uint8)
+        b = np.frombuffer(s_ref, np.uint8)
+        i = int(np.nonzero(a != b)[0][0])
+        raise AssertionError("stream differs first at byte %d of %d" % (i, len(a)))
+    assert st == 0
+    assert torch.equal(y, x_dev)
+
+
+# ------------------------------------------------------------------ small cases
+EDGE = [
+    # (values, dtype, L)
+    ([5, 7, 6, 4, 4, 4, 4], np.uint16, 3),
+    ([42], np.uint16, 0),
+    ([42], np.uint32, 1),
+    ([0, 65535], np.uint16, 0),              # B = 2^16 -> pow2, k = 4
+    ([0, 0xFFFFFFFF], np.uint32, 0),         # B = 2^32 -> pow2, k = 2
+    ([0xFFFFFFFF] * 9, np.uint32, 4),        # constant at the top
+    ([65535] * 1000, np.uint16, 7),          # all 65535
+    (list(range(16)) * 40, np.uint16, 64),   # B = 16
+    (list(range(256)) * 9, np.uint16, 300),  # B = 256
+    (list(range(3)) * 333, np.uint16, 0),    # B = 3, k = 40
+    ([1, 2, 3], np.uint16, 10),              # L > n
+]
+
+
+@pytest.mark.parametrize("idx", range(len(EDGE)))
+def test_edge_matrix(oracle_lib, idx):
+    v, dt, L = EDGE[idx]
+    check_case(oracle_lib, np.array(v, dtype=dt), L)
+
+
+def test_random_small_shapes(oracle_lib):
+    rng = np.random.default_rng(123)
+    for it in range(300):
+        w = 16 if it % 3 else 32
+        n = int(rng.integers(1, 5000))
+        kind = it % 6
+        hi = 1 << w
+        if kind == 0:
+            base = int(rng.integers(0, hi - 100000)) if w == 32 else int(rng.integers(0, hi - 200))
+            x = rng.integers(base, base + int(rng.integers(1, 200)), size=n, dtype=np.uint64)
+        elif kind == 1:
+            x = rng.integers(0, hi, size=n, dtype=np.uint64)
+        elif kind == 2:
+            j = int(rng.integers(1, w + 1))
+            x = rng.integers(0, 1 << j, size=n, dtype=np.uint64)
+        elif kind == 3:
+            x = np.full(n, int(rng.integers(0, hi)), dtype=np.uint64)
+        elif kind == 4:
+            x = rng.integers(1000, 1040, size=n, dtype=np.uint64)
+            x[rng.integers(0, n, size=max(1, n // 500))] = hi - 1
+        else:
+            b = int(rng.integers(2, 1 << min(w, 22)))
+            x = rng.integers(0, b, size=n, dtype=np.uint64)
+        L = int(rng.choice([0, 1, 2, 3, 5, 7, 30, 31, 64, 100, 154, 1000, 1024, 4096, 5000, 9000, 20000]))
+        check_case(oracle_lib, x.astype(np.uint16 if w == 16 else np.uint32), L)
+
+
+def test_every_u16_base_decodes(oracle_lib):
+    """Each block of 64 values spans exactly base B (0 and B-1 present), for
+    every B in 2..65536 in turn: exercises every table entry of both sides."""
+    rng = np.random.default_rng(5)
+    B = np.arange(2, 65537, dtype=np.int64)
+    L = 64
+    d = rng.integers(0, 1 << 62, size=(B.size, L), dtype=np.int64) % B[:, None]
+    d[:, 0] = 0
+    d[:, 1] = B - 1
+    off = rng.integers(0, 65536, size=B.size) % (65537 - B)
+    x = (d + off[:, None]).astype(np.uint16).reshape(-1)
+    check_case(oracle_lib, x, L)
+
+
+def test_large_bases_u32(oracle_lib):
+    rng = np.random.default_rng(9)
+    Bs = [65537, 65539, 100003, 1 << 20, (1 << 20) + 7, 2642245, 2642246, 3 * 10 ** 6, (1 << 31) + 11,
+          (1 << 32) - 1, 1 << 32]
+    blocks = []
+    for B in Bs:
+        blk = rng.integers(0, B, size=77, dtype=np.uint64)
+        blk[0], blk[1] = 0, B - 1
+        blocks.append(blk)
+    x = np.concatenate(blocks).astype(np.uint32)
+    check_case(oracle_lib, x, 77)
+    check_case(oracle_lib, x, 0)
+
+
+# ------------------------------------------------------------------ configs
+SMALL = {1: 1.0, 2: 1 / 100, 3: 1 / 64, 4: 1 / 128, 5: 1 / 128}
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_config_scaled(oracle_lib, cfg):
+    c = workloads.config(cfg, SMALL[cfg])
+    x = workloads.generate(cfg, scale=SMALL[cfg], seed=1, device="cuda")
+    s_gpu, y, st = gpu_roundtrip(x, c.block_len)
+    s_ref = oracle_lib.compress(x.cpu().numpy(), c.block_len)
+    assert s_gpu == s_ref
+    assert st == 0 and torch.equal(y, x)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_config_full_size(oracle_lib, cfg):
+    """BASELINE.json full sizes, in the launch configuration bench.py times:
+    the whole stream equals the oracle's, and decompress(compress(x)) == x."""
+    c = workloads.config(cfg, 1.0)
+    x = workloads.generate(cfg, scale=1.0, seed=0, device="cuda")
+    out, nb = pc.poly_compress(x, c.block_len)
+    nbytes = int(nb.item())
+    s_ref = oracle_lib.compress(x.cpu().numpy(), c.block_len)
+    assert nbytes == len(s_ref)
+    ref_dev = torch.from_numpy(np.frombuffer(s_ref, dtype=np.uint8).copy()).cuda()
+    assert torch.equal(out[:nbytes], ref_dev)
+    del ref_dev
+    y, st = pc.poly_decompress(out, nbytes, 16 if c.dtype == torch.uint16 else 32, c.n, c.block_len)
+    assert int(st.item()) == 0
+    assert torch.equal(y, x)
+
+
+# ------------------------------------------------------------------ corruption
+def _stream(x, L):
+    x_dev = to_dev(np.array(x, dtype=np.uint16))
+    return pc.compress(x_dev, L).cpu().numpy().tobytes()
+
+
+def _status(buf: bytes, n, L, dt=16, nbytes=None):
+    d = torch.from_numpy(np.frombuffer(buf + bytes(64), dtype=np.uint8).copy()).cuda()
+    _, st = pc.poly_decompress(d, len(buf) if nbytes is None else nbytes, dt, n, L)
+    return int(st.item())
+
+
+@pytest.mark.parametrize("large", [False, True])
+def test_corruption_status_bits(large):
+    x = [5, 7, 6, 4, 4, 4, 4] if not large else list(np.arange(20000) % 37)
+    L = 3 if not large else 10000
+    n = len(x)
+    s = _stream(x, L)
+    nbl = (n + L - 1) // L
+    assert _status(s, n, L) == 0
+    assert _status(b"XXXX" + s[4:], n, L) & pc.POLY_ST_BAD_MAGIC
+    assert _status(s[:4] + b"\x01" + s[5:], n, L) & pc.POLY_ST_BAD_VERSION
+    assert _status(s, n + 1, L) & pc.POLY_ST_HEADER_MISMATCH
+    assert _status(s, n, L, dt=32) & pc.POLY_ST_HEADER_MISMATCH
+    assert _status(s, n, L, nbytes=len(s) - 8) & pc.POLY_ST_LENGTH
+    assert _status(s[:32] + struct.pack("<I", 9) + s[36:], n, L) & pc.POLY_ST_BAD_CODEC
+    assert _status(s[:44] + struct.pack("<I", 5) + s[48:], n, L) & (pc.POLY_ST_NWORDS | pc.POLY_ST_LENGTH)
+    assert _status(s[:36] + struct.pack("<I", 65535) + s[40:], n, L) & pc.POLY_ST_OVERFLOW
+    pay = 32 + 16 * nbl
+    bad_word = struct.pack("<Q", (1 << 64) - 1)
+    assert _status(s[:pay] + bad_word + s[pay + 8:], n, L) & pc.POLY_ST_RESIDUE
+
+
+def test_empty_input_rejected():
+    x = torch.empty(0, dtype=torch.uint16, device="cuda")
+    with pytest.raises(pc.PolyError) as e:
+        pc.poly_compress(x, 0)
+    assert e.value.code == 2
