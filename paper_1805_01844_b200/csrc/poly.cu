@@ -8,12 +8,13 @@
 #include "poly_common.cuh"
 #include "poly_compress.cuh"
 #include "poly_decompress.cuh"
+#include "poly_warp.cuh"
 
 using namespace polyk;
 
 namespace {
 
-enum Regime { TILED = 0, LARGE = 1 };
+enum Regime { WARP = 0, LARGE = 1 };
 
 constexpr int MAX_DEVICES = 64;
 std::mutex g_mu;
@@ -73,8 +74,6 @@ void set_smem_attr(K kernel, int bytes) {
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
-uint32_t tiled_smem_compress(uint32_t T) { return TILE_BYTES + 8 * MAX_WORDS + 16 * T; }
-uint32_t tiled_smem_decompress(uint32_t T) { return TILE_BYTES + 8 * MAX_WORDS + 60 * T; }
 template <typename V>
 uint32_t large_smem_pack() { return ((CH_VALUES + 64) * sizeof(V) + 15) / 16 * 16; }
 template <typename V>
@@ -93,11 +92,15 @@ poly_status_t ensure_init(int dev) {
   cudaError_t e = cudaMemcpyToSymbol(g_ktab, h_ktab, sizeof h_ktab);
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_dtab, h_dtab, sizeof h_dtab);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
-  const int tc = tiled_smem_compress(T_MAX), td = tiled_smem_decompress(T_MAX);
-  set_smem_attr(poly_compress_tiled<uint16_t>, tc);
-  set_smem_attr(poly_compress_tiled<uint32_t>, tc);
-  set_smem_attr(poly_decompress_tiled<uint16_t>, td);
-  set_smem_attr(poly_decompress_tiled<uint32_t>, td);
+  const int wmax = WARPS * (WT_MAX + 512);
+  set_smem_attr(poly_compress_warp<uint16_t, 0>, wmax);
+  set_smem_attr(poly_compress_warp<uint16_t, 1>, wmax);
+  set_smem_attr(poly_compress_warp<uint32_t, 0>, wmax);
+  set_smem_attr(poly_compress_warp<uint32_t, 1>, wmax);
+  set_smem_attr(poly_decompress_warp<uint16_t, 0>, wmax);
+  set_smem_attr(poly_decompress_warp<uint16_t, 1>, wmax);
+  set_smem_attr(poly_decompress_warp<uint32_t, 0>, wmax);
+  set_smem_attr(poly_decompress_warp<uint32_t, 1>, wmax);
   set_smem_attr(poly_compress_pack<uint16_t>, large_smem_pack<uint16_t>());
   set_smem_attr(poly_compress_pack<uint32_t>, large_smem_pack<uint32_t>());
   set_smem_attr(poly_decompress_unpack<uint16_t>, large_smem_unpack<uint16_t>());
@@ -120,38 +123,37 @@ uint32_t gcd32(uint32_t a, uint32_t b) {
 
 // Regime and launch shape for (n, w, block_size).  Deterministic: the same
 // arguments always give the same shape (the stream does not depend on it).
-bool plan(uint64_t n, uint32_t w, uint64_t block_size, Shape& sh, Regime& rg) {
+constexpr uint32_t WT_TARGET = 4096;  // input bytes per warp unit (target)
+
+bool plan(uint64_t n, uint32_t w, uint64_t block_size, Shape& sh, WarpShape& ws, Regime& rg) {
   if (n == 0 || (w != 16 && w != 32) || block_size >= (1ull << 32)) return false;
   memset(&sh, 0, sizeof sh);
+  memset(&ws, 0, sizeof ws);
   sh.n = n;
   sh.width = w;
   sh.block_len = (uint32_t)block_size;
   sh.Le = block_size == 0 ? n : block_size;
   sh.n_blocks = (n + sh.Le - 1) / sh.Le;
   if (sh.n_blocks >= (1ull << 32)) return false;
-  const uint32_t vb = w / 8;
-  const uint64_t TV = TILE_BYTES / vb;
-  if (sh.Le <= TV) {
-    rg = TILED;
-    const uint64_t kmin = w == 16 ? 4 : 2;
-    uint64_t T = TV / sh.Le;
-    T = std::min<uint64_t>(T, T_MAX);
-    T = std::min<uint64_t>(T, MAX_WORDS / ((sh.Le + kmin - 1) / kmin));
-    if (T >= (uint64_t)NT) {
-      T = T / NT * NT;
+  const uint64_t bb = sh.Le * (w / 8);  // bytes per block
+  if (bb <= WT_MAX) {
+    rg = WARP;
+    ws.n = n; ws.Le = sh.Le; ws.n_blocks = sh.n_blocks; ws.block_len = sh.block_len; ws.width = w;
+    if (bb <= LANE_BLOCK_MAX) {
+      ws.mode = 0;
+      uint64_t bpl = WT_TARGET / (32 * bb);
+      bpl = std::max<uint64_t>(1, std::min<uint64_t>(4, bpl));
+      ws.WB = (uint32_t)(32 * bpl);
+      ws.slice = (uint32_t)((ws.WB * bb + 15) / 16 * 16);
     } else {
-      const uint64_t ta = 16 / gcd32(16, (uint32_t)((sh.Le * vb) % 16 ? (sh.Le * vb) % 16 : 16));
-      if (T >= ta) T = T / ta * ta;
+      ws.mode = 1;
+      uint64_t wb = WT_TARGET / bb;
+      wb = std::max<uint64_t>(1, std::min<uint64_t>(32, wb));
+      ws.WB = (uint32_t)wb;
+      ws.slice = (uint32_t)((ws.WB * bb + 15) / 16 * 16 + 512);
     }
-    if (T < 1) T = 1;
-    sh.T = (uint32_t)T;
-    uint32_t G = 1;
-    if (T < (uint64_t)NT) {
-      const uint32_t q = (uint32_t)(NT / T);
-      while (G * 2 <= q) G *= 2;
-    }
-    sh.G = G;
-    sh.n_tiles = (sh.n_blocks + T - 1) / T;
+    ws.n_units = (sh.n_blocks + ws.WB - 1) / ws.WB;
+    if (ws.n_units >= (1ull << 32)) return false;
   } else {
     rg = LARGE;
     sh.cpb = (sh.Le + CH_VALUES - 1) / CH_VALUES;
@@ -165,12 +167,12 @@ struct WsLayout {
   uint64_t status_off, bmin_off, bmax_off, woff_off, total;
 };
 
-WsLayout ws_layout(const Shape& sh, Regime rg) {
+WsLayout ws_layout(const Shape& sh, const WarpShape& ws, Regime rg) {
   WsLayout L;
   memset(&L, 0, sizeof L);
   L.status_off = 64;
-  if (rg == TILED) {
-    L.total = 64 + 8 * sh.n_tiles;
+  if (rg == WARP) {
+    L.total = 64 + 8 * ws.n_units;
   } else {
     L.bmin_off = (64 + 8 * sh.n_stiles + 15) / 16 * 16;
     L.bmax_off = (L.bmin_off + 4 * sh.n_blocks + 15) / 16 * 16;
@@ -189,6 +191,18 @@ int current_device() {
 int grid_for(uint64_t work, int dev) {
   const uint64_t cap = (uint64_t)(g_sms[dev] > 0 ? g_sms[dev] : 148) * 8;
   return (int)std::min<uint64_t>(work, cap);
+}
+
+// Persistent grid for a warp-tile kernel: every resident CTA, capped by work.
+template <typename K>
+int warp_grid(K kernel, uint32_t smem, uint64_t units, int dev) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, WARPS * 32, smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  const uint64_t cap = (uint64_t)(g_sms[dev] > 0 ? g_sms[dev] : 148) * per_sm;
+  const uint64_t need = (units + WARPS - 1) / WARPS;
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>(cap, need));
 }
 
 }  // namespace
@@ -225,16 +239,18 @@ uint64_t poly_max_compressed_bytes(uint64_t n, poly_dtype_t dt, uint64_t block_s
 
 uint64_t poly_workspace_bytes(uint64_t n, poly_dtype_t dt, uint64_t block_size) {
   Shape sh;
+  WarpShape ws;
   Regime rg;
-  if (!plan(n, (uint32_t)dt, block_size, sh, rg)) return 0;
-  return ws_layout(sh, rg).total;
+  if (!plan(n, (uint32_t)dt, block_size, sh, ws, rg)) return 0;
+  return ws_layout(sh, ws, rg).total;
 }
 
 int poly_launches_per_call(uint64_t n, poly_dtype_t dt, uint64_t block_size, int decompress) {
   Shape sh;
+  WarpShape ws;
   Regime rg;
-  if (!plan(n, (uint32_t)dt, block_size, sh, rg)) return 0;
-  if (rg == TILED) return 1;
+  if (!plan(n, (uint32_t)dt, block_size, sh, ws, rg)) return 0;
+  if (rg == WARP) return 1;
   return decompress ? 2 : 3;
 }
 
@@ -250,10 +266,11 @@ poly_status_t poly_compress(const void* d_in, uint64_t n, poly_dtype_t dt, uint6
   if ((reinterpret_cast<uintptr_t>(d_compressed_bytes) & 7) != 0) return POLY_ERR_INVALID_ARG;
   if ((reinterpret_cast<uintptr_t>(d_workspace) & 15) != 0) return POLY_ERR_INVALID_ARG;
   Shape sh;
+  WarpShape wsh;
   Regime rg;
-  if (!plan(n, (uint32_t)dt, block_size, sh, rg)) return POLY_ERR_INVALID_ARG;
+  if (!plan(n, (uint32_t)dt, block_size, sh, wsh, rg)) return POLY_ERR_INVALID_ARG;
   if (out_capacity < poly_max_compressed_bytes(n, dt, block_size)) return POLY_ERR_CAPACITY;
-  const WsLayout W = ws_layout(sh, rg);
+  const WsLayout W = ws_layout(sh, wsh, rg);
   if (workspace_bytes < W.total) return POLY_ERR_WORKSPACE;
   const int dev = current_device();
   poly_status_t st = ensure_init(dev);
@@ -269,13 +286,20 @@ poly_status_t poly_compress(const void* d_in, uint64_t n, poly_dtype_t dt, uint6
   a.ticket = reinterpret_cast<uint32_t*>(ws);
   a.status = reinterpret_cast<uint64_t*>(ws + W.status_off);
   a.sh = sh;
-  if (rg == TILED) {
+  if (rg == WARP) {
     cudaMemsetAsync(ws, 0, W.total, s);
-    const uint32_t smem = tiled_smem_compress(sh.T);
-    if (dt == POLY_U16)
-      poly_compress_tiled<uint16_t><<<(unsigned)sh.n_tiles, NT, smem, s>>>(a);
-    else
-      poly_compress_tiled<uint32_t><<<(unsigned)sh.n_tiles, NT, smem, s>>>(a);
+    WarpArgs wa;
+    memset(&wa, 0, sizeof wa);
+    wa.in = reinterpret_cast<const uint8_t*>(d_in);
+    wa.out = a.out;
+    wa.compressed_bytes = d_compressed_bytes;
+    wa.status = a.status;
+    wa.ticket = a.ticket;
+    wa.sh = wsh;
+    const uint32_t smem = WARPS * wsh.slice;
+    auto k = dt == POLY_U16 ? (wsh.mode == 0 ? poly_compress_warp<uint16_t, 0> : poly_compress_warp<uint16_t, 1>)
+                            : (wsh.mode == 0 ? poly_compress_warp<uint32_t, 0> : poly_compress_warp<uint32_t, 1>);
+    k<<<warp_grid(k, smem, wsh.n_units, dev), WARPS * 32, smem, s>>>(wa);
   } else {
     a.bmin = reinterpret_cast<uint32_t*>(ws + W.bmin_off);
     a.bmax = reinterpret_cast<uint32_t*>(ws + W.bmax_off);
@@ -329,9 +353,10 @@ poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_
   if ((reinterpret_cast<uintptr_t>(d_out) % vb) != 0) return POLY_ERR_INVALID_ARG;
   if ((reinterpret_cast<uintptr_t>(d_workspace) & 15) != 0) return POLY_ERR_INVALID_ARG;
   Shape sh;
+  WarpShape wsh;
   Regime rg;
-  if (!plan(n, (uint32_t)dt, block_size, sh, rg)) return POLY_ERR_INVALID_ARG;
-  const WsLayout W = ws_layout(sh, rg);
+  if (!plan(n, (uint32_t)dt, block_size, sh, wsh, rg)) return POLY_ERR_INVALID_ARG;
+  const WsLayout W = ws_layout(sh, wsh, rg);
   if (workspace_bytes < W.total) return POLY_ERR_WORKSPACE;
   const int dev = current_device();
   poly_status_t st = ensure_init(dev);
@@ -349,13 +374,22 @@ poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_
   a.status = reinterpret_cast<uint64_t*>(ws + W.status_off);
   a.sh = sh;
   cudaMemsetAsync(d_status, 0, 4, s);
-  if (rg == TILED) {
+  if (rg == WARP) {
     cudaMemsetAsync(ws, 0, W.total, s);
-    const uint32_t smem = tiled_smem_decompress(sh.T);
-    if (dt == POLY_U16)
-      poly_decompress_tiled<uint16_t><<<(unsigned)sh.n_tiles, NT, smem, s>>>(a);
-    else
-      poly_decompress_tiled<uint32_t><<<(unsigned)sh.n_tiles, NT, smem, s>>>(a);
+    WarpArgs wa;
+    memset(&wa, 0, sizeof wa);
+    wa.in = a.in;
+    wa.out = reinterpret_cast<uint8_t*>(d_out);
+    wa.in_bytes = compressed_bytes;
+    wa.status_out = d_status;
+    wa.status = a.status;
+    wa.ticket = a.ticket;
+    wa.sh = wsh;
+    const uint32_t smem = WARPS * wsh.slice;
+    auto k = dt == POLY_U16
+                 ? (wsh.mode == 0 ? poly_decompress_warp<uint16_t, 0> : poly_decompress_warp<uint16_t, 1>)
+                 : (wsh.mode == 0 ? poly_decompress_warp<uint32_t, 0> : poly_decompress_warp<uint32_t, 1>);
+    k<<<warp_grid(k, smem, wsh.n_units, dev), WARPS * 32, smem, s>>>(wa);
   } else {
     a.woff = reinterpret_cast<uint64_t*>(ws + W.woff_off);
     cudaMemsetAsync(ws, 0, W.bmin_off, s);

@@ -12,9 +12,6 @@ namespace polyk {
 
 constexpr int NT = 256;                 // threads per CTA (8 warps)
 constexpr int NWARP = NT / 32;
-constexpr uint32_t TILE_BYTES = 16384;  // input bytes staged per tiled CTA
-constexpr uint32_t MAX_WORDS = 2560;    // payload words staged per tile (20 KiB)
-constexpr uint32_t T_MAX = 512;         // blocks per tile
 constexpr uint32_t CH_VALUES = 8192;    // values per chunk in the large-block regime
 constexpr uint32_t KTAB_MAX = 65536;    // B <= KTAB_MAX use the tables
 
@@ -239,9 +236,6 @@ struct Shape {
   uint64_t n_blocks;
   uint32_t block_len;   // as given (0 = whole), stored in the global header
   uint32_t width;       // 16 or 32
-  uint32_t T;           // blocks per tile (tiled regime)
-  uint32_t G;           // threads per block group (tiled regime), power of two
-  uint64_t n_tiles;     // tiled regime
   uint64_t cpb;         // chunks per block (large regime)
   uint64_t n_chunks;    // large regime
   uint64_t n_stiles;    // scan tiles over blocks (large regime)

@@ -1,13 +1,9 @@
 // poly_compress.cuh -- compress kernels.
 //
-// Tiled regime (block_len * w <= TILE_BYTES): one CTA per tile of T whole
-// blocks, tiles handed out by an atomic ticket.  Single pass over the input:
-//   load tile (16-byte loads) -> per-block min/max (a2) -> B, k, n_words (a3)
-//   -> CTA scan of n_words + publish tile aggregate -> Horner pack into smem
-//   (a5) -> decoupled look-back for the tile's payload offset (a4) -> headers
-//   and coalesced payload stores (a6); the last tile writes the global header.
-// Large regime (longer blocks, e.g. cfg1 / cfg3): chunked min/max with
-// atomics, a look-back scan over blocks, then a chunked pack pass.
+// Large-block regime (block_len * w > WT_MAX, e.g. cfg1 / cfg3): chunked
+// min/max with atomics (a2), a look-back scan over blocks for B, k, n_words,
+// headers and payload offsets (a3, a4, a6), then a chunked Horner pack pass
+// (a5).  Blocks up to WT_MAX bytes use the warp-tile kernels (poly_warp.cuh).
 #pragma once
 #include "poly_common.cuh"
 
@@ -17,7 +13,7 @@ struct CompressArgs {
   const void* in;
   uint8_t* out;
   uint64_t* compressed_bytes;
-  uint64_t* status;   // n_tiles (tiled) or n_stiles (large) look-back words
+  uint64_t* status;   // n_stiles look-back words
   uint32_t* ticket;
   uint32_t* bmin;     // large regime: per-block running min
   uint32_t* bmax;     // large regime: per-block running max
@@ -47,119 +43,6 @@ __device__ __forceinline__ uint64_t horner_word(const V* v, uint32_t m, uint64_t
   uint64_t s = 0;
   for (int i = (int)m - 1; i >= 0; --i) s = s * B + (uint64_t)((uint32_t)v[i] - vmin);
   return s;
-}
-
-template <typename V>
-__global__ void __launch_bounds__(NT) poly_compress_tiled(CompressArgs a) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const Shape& sh = a.sh;
-  V* s_in = reinterpret_cast<V*>(smem);
-  uint64_t* s_words = reinterpret_cast<uint64_t*>(smem + TILE_BYTES);
-  uint32_t* s_vmin = reinterpret_cast<uint32_t*>(smem + TILE_BYTES + 8 * MAX_WORDS);
-  uint32_t* s_bm1 = s_vmin + sh.T;   // holds v_max until the B stage
-  uint32_t* s_nw = s_bm1 + sh.T;
-  uint32_t* s_woff = s_nw + sh.T;
-  __shared__ uint32_t s_tile;
-  __shared__ uint32_t s_warp[NWARP];
-  __shared__ uint64_t s_prefix;
-
-  const int tid = threadIdx.x;
-  if (tid == 0) s_tile = atomicAdd(a.ticket, 1u);
-  __syncthreads();
-  const uint64_t tile = s_tile;
-  const uint64_t b0 = tile * sh.T;
-  const uint32_t nblk = (uint32_t)min((uint64_t)sh.T, sh.n_blocks - b0);
-  const uint64_t v0 = b0 * sh.Le;
-  const uint32_t nv = (uint32_t)(min(sh.n, v0 + (uint64_t)sh.T * sh.Le) - v0);
-  const uint32_t L = (uint32_t)sh.Le;
-
-  // (a1) stage the tile
-  load_values<V>(s_in, reinterpret_cast<const V*>(a.in) + v0, nv);
-  const uint32_t G = sh.G;
-  if (G > 32)
-    for (uint32_t b = tid; b < nblk; b += NT) { s_vmin[b] = 0xffffffffu; s_bm1[b] = 0u; }
-  __syncthreads();
-
-  // (a2) per-block min/max by groups of G threads
-  const uint32_t groups = NT / G, gid = tid / G, g = tid % G;
-  const uint32_t rounds = (nblk + groups - 1) / groups;
-  for (uint32_t r = 0; r < rounds; ++r) {
-    const uint32_t b = r * groups + gid;
-    const bool active = b < nblk;
-    uint32_t mn = 0xffffffffu, mx = 0u;
-    if (active) {
-      const uint32_t lo = b * L, nb = min(L, nv - lo);
-      for (uint32_t i = g; i < nb; i += G) {
-        const uint32_t v = (uint32_t)s_in[lo + i];
-        mn = min(mn, v);
-        mx = max(mx, v);
-      }
-    }
-    const int w = G < 32 ? (int)G : 32;
-    mn = shfl_min(mn, w);
-    mx = shfl_max(mx, w);
-    if (active) {
-      if (G <= 32) {
-        if (g == 0) { s_vmin[b] = mn; s_bm1[b] = mx; }
-      } else if ((tid & 31) == 0) {
-        atomicMin(&s_vmin[b], mn);
-        atomicMax(&s_bm1[b], mx);
-      }
-    }
-  }
-  __syncthreads();
-
-  // (a3) base B, capacity k, word count
-  for (uint32_t b = tid; b < nblk; b += NT) {
-    const uint32_t nb = min(L, nv - b * L);
-    const uint64_t B = (uint64_t)s_bm1[b] - s_vmin[b] + 1;
-    s_bm1[b] = (uint32_t)(B - 1);
-    s_nw[b] = B == 1 ? 0u : (nb + capacity_of(B) - 1) / capacity_of(B);
-  }
-  __syncthreads();
-
-  // (a4) tile-local offsets, publish the aggregate early
-  const uint32_t total = cta_exclusive_scan<uint32_t>(s_nw, s_woff, nblk, s_warp);
-  if (tid == 0) st_relaxed_u64(a.status + tile, (tile == 0 ? FLAG_PRE : FLAG_AGG) | total);
-
-  // (a5) Horner pack into smem
-  for (uint32_t b = gid; b < nblk; b += groups) {
-    const uint32_t bm1 = s_bm1[b];
-    if (bm1 == 0) continue;
-    const uint64_t B = (uint64_t)bm1 + 1;
-    const uint32_t k = capacity_of(B);
-    const uint32_t lo = b * L, nb = min(L, nv - lo), nw = s_nw[b], base = s_woff[b];
-    const uint32_t vmin = s_vmin[b];
-    for (uint32_t j = g; j < nw; j += G) {
-      const uint32_t first = j * k;
-      s_words[base + j] = horner_word<V>(s_in + lo + first, min(k, nb - first), B, vmin);
-    }
-  }
-
-  // (a4) look-back for the tile's global word offset
-  if (tid < 32) {
-    uint64_t p = 0;
-    if (tile != 0) {
-      p = lookback(a.status, tile);
-      if (tid == 0) st_relaxed_u64(a.status + tile, FLAG_PRE | (p + total));
-    }
-    if (tid == 0) s_prefix = p;
-  }
-  __syncthreads();
-  const uint64_t P = s_prefix;
-
-  // (a6) emit headers and payload
-  uint4* hdr = reinterpret_cast<uint4*>(a.out + 32) + b0;
-  for (uint32_t b = tid; b < nblk; b += NT) {
-    const uint32_t bm1 = s_bm1[b];
-    hdr[b] = make_uint4(bm1 == 0 ? CODEC_CONSTANT : CODEC_BASIC, s_vmin[b], bm1, s_nw[b]);
-  }
-  uint64_t* dst = reinterpret_cast<uint64_t*>(a.out + 32 + 16 * sh.n_blocks) + P;
-  for (uint32_t i = tid; i < total; i += NT) dst[i] = s_words[i];
-  if (tile == sh.n_tiles - 1 && tid == 0) {
-    write_global_header(a.out, sh, P + total);
-    *a.compressed_bytes = 32 + 16 * sh.n_blocks + 8 * (P + total);
-  }
 }
 
 // ------------------------------------------------------------ large regime

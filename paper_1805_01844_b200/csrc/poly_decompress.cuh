@@ -9,6 +9,7 @@
 // multiply-adds per digit.  Power-of-two bases use shifts and masks.
 #pragma once
 #include "poly_common.cuh"
+#include "poly_warp.cuh"
 
 namespace polyk {
 
@@ -55,151 +56,6 @@ __device__ __forceinline__ uint32_t check_block(uint4 h, uint64_t nb, uint32_t w
   if (h.z == 0 || (uint64_t)h.y + h.z > vmax_allowed) return POLY_ST_OVERFLOW;
   if ((uint64_t)h.w != (nb + k - 1) / k) return POLY_ST_NWORDS;
   return 0;
-}
-
-// Decode one word into out[0..m); returns POLY_ST_RESIDUE if the word holds
-// more than m digits (or is >= B^k).
-template <typename V>
-__device__ __forceinline__ uint32_t decode_word(uint64_t s, const DecConst& c, uint64_t B, uint32_t m,
-                                                uint32_t vmin, V* out) {
-  if (c.log2b) {
-    const uint32_t j = c.log2b;
-    const uint64_t mask = (1ull << j) - 1;
-    for (uint32_t i = 0; i < m; ++i) out[i] = (V)(vmin + (uint32_t)((s >> (i * j)) & mask));
-    return (m * j < 64 && (s >> (m * j)) != 0) ? POLY_ST_RESIDUE : 0u;
-  }
-  if (s >= c.Bk) return POLY_ST_RESIDUE;
-  const uint64_t hi1 = __umul64hi(s, c.Rl);
-  const uint64_t lo2 = s * c.Rh;
-  const uint64_t hi2 = __umul64hi(s, c.Rh);
-  const uint64_t mid = lo2 + hi1;
-  const uint64_t carry = mid < lo2 ? 1ull : 0ull;
-  uint64_t f = ((hi2 + carry) << 32) + (mid >> 32) + 1;
-  uint32_t extra = 0;
-  for (int i = (int)c.k - 1; i >= 0; --i) {
-    const uint64_t t0 = (uint64_t)(uint32_t)f * B;
-    const uint64_t t1 = (f >> 32) * B + (t0 >> 32);
-    const uint32_t d = (uint32_t)(t1 >> 32);
-    f = (t1 << 32) | (uint32_t)t0;
-    if ((uint32_t)i < m) out[i] = (V)(vmin + d);
-    else extra |= d;
-  }
-  return extra ? POLY_ST_RESIDUE : 0u;
-}
-
-template <typename V>
-__global__ void __launch_bounds__(NT) poly_decompress_tiled(DecompressArgs a) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const Shape& sh = a.sh;
-  V* s_out = reinterpret_cast<V*>(smem);
-  uint64_t* s_words = reinterpret_cast<uint64_t*>(smem + TILE_BYTES);
-  DecConst* s_cst = reinterpret_cast<DecConst*>(smem + TILE_BYTES + 8 * MAX_WORDS);
-  uint64_t* s_nw = reinterpret_cast<uint64_t*>(s_cst + sh.T);
-  uint64_t* s_woff = s_nw + sh.T;
-  uint32_t* s_vmin = reinterpret_cast<uint32_t*>(s_woff + sh.T);
-  uint32_t* s_bm1 = s_vmin + sh.T;
-  uint32_t* s_ok = s_bm1 + sh.T;   // 0 invalid, 1 constant, 2 basic
-  __shared__ uint32_t s_tile, s_err, s_hdr_err;
-  __shared__ uint64_t s_warp[NWARP];
-  __shared__ uint64_t s_prefix, s_pw;
-
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    s_tile = atomicAdd(a.ticket, 1u);
-    s_err = 0;
-    uint64_t pw = 0;
-    s_hdr_err = check_global_header(a, &pw);
-    s_pw = pw;
-  }
-  __syncthreads();
-  const uint64_t tile = s_tile;
-  if (s_hdr_err) {  // same verdict in every CTA: nothing is decoded
-    if (tile == 0 && tid == 0) atomicOr(a.status_out, s_hdr_err);
-    return;
-  }
-  const uint64_t payload_words = s_pw;
-  const uint64_t b0 = tile * sh.T;
-  const uint32_t nblk = (uint32_t)min((uint64_t)sh.T, sh.n_blocks - b0);
-  const uint64_t v0 = b0 * sh.Le;
-  const uint32_t nv = (uint32_t)(min(sh.n, v0 + (uint64_t)sh.T * sh.Le) - v0);
-  const uint32_t L = (uint32_t)sh.Le;
-
-  // (a7) headers of this tile
-  const uint4* hdr = reinterpret_cast<const uint4*>(a.in + 32) + b0;
-  uint32_t err = 0;
-  for (uint32_t b = tid; b < nblk; b += NT) {
-    const uint4 h = hdr[b];
-    const uint32_t nb = min(L, nv - b * L);
-    uint32_t ok = 0;
-    if (h.x == CODEC_BASIC && h.z != 0) {
-      const DecConst c = dec_const_of((uint64_t)h.z + 1);
-      s_cst[b] = c;
-      const uint32_t e = check_block(h, nb, sh.width, c.k);
-      err |= e;
-      ok = e ? 0u : 2u;
-    } else {
-      const uint32_t e = check_block(h, nb, sh.width, 1);
-      err |= e;
-      ok = e ? 0u : 1u;
-    }
-    s_nw[b] = h.w;
-    s_vmin[b] = h.y;
-    s_bm1[b] = h.z;
-    s_ok[b] = ok;
-  }
-  if (err) atomicOr(&s_err, err);
-  __syncthreads();
-
-  // (a7) offsets: CTA scan + look-back
-  const uint64_t total = cta_exclusive_scan<uint64_t>(s_nw, s_woff, nblk, s_warp);
-  if (tid < 32) {
-    uint64_t p = 0;
-    if (tid == 0) st_relaxed_u64(a.status + tile, (tile == 0 ? FLAG_PRE : FLAG_AGG) | (total & VAL_MASK));
-    if (tile != 0) {
-      p = lookback(a.status, tile);
-      if (tid == 0) st_relaxed_u64(a.status + tile, FLAG_PRE | ((p + total) & VAL_MASK));
-    }
-    if (tid == 0) {
-      s_prefix = p;
-      if (p + total > payload_words || total > MAX_WORDS) atomicOr(&s_err, POLY_ST_LENGTH);
-      if (tile == sh.n_tiles - 1 && p + total != payload_words) atomicOr(&s_err, POLY_ST_LENGTH);
-    }
-  }
-  __syncthreads();
-  const uint64_t P = s_prefix;
-  const uint64_t avail = P < payload_words ? payload_words - P : 0;
-  const uint32_t nload = (uint32_t)min(min(total, (uint64_t)MAX_WORDS), avail);
-
-  // payload words of the tile
-  const uint64_t* pay = reinterpret_cast<const uint64_t*>(a.in + 32 + 16 * sh.n_blocks) + P;
-  for (uint32_t i = tid; i < nload; i += NT) s_words[i] = ldg_nc_u64(pay + i);
-  __syncthreads();
-
-  // (a8) digit extraction by groups of G threads per block
-  const uint32_t G = sh.G, groups = NT / G, gid = tid / G, g = tid % G;
-  for (uint32_t b = gid; b < nblk; b += groups) {
-    const uint32_t ok = s_ok[b];
-    if (!ok) continue;
-    const uint32_t lo = b * L, nb = min(L, nv - lo), vmin = s_vmin[b];
-    if (ok == 1) {
-      for (uint32_t i = g; i < nb; i += G) s_out[lo + i] = (V)vmin;
-      continue;
-    }
-    const DecConst c = s_cst[b];
-    const uint64_t B = (uint64_t)s_bm1[b] + 1;
-    const uint32_t nw = (uint32_t)s_nw[b];
-    const uint64_t base = s_woff[b];
-    for (uint32_t j = g; j < nw; j += G) {
-      if (base + j >= nload) break;
-      const uint32_t first = j * c.k;
-      err |= decode_word<V>(s_words[base + j], c, B, min(c.k, nb - first), vmin, s_out + lo + first);
-    }
-  }
-  if (err) atomicOr(&s_err, err);
-  __syncthreads();
-
-  store_values<V>(reinterpret_cast<V*>(a.out) + v0, s_out, nv);
-  if (tid == 0 && s_err) atomicOr(a.status_out, s_err);
 }
 
 // ------------------------------------------------------------ large regime
@@ -313,8 +169,8 @@ __global__ void __launch_bounds__(NT) poly_decompress_unpack(DecompressArgs a) {
     const uint64_t f0 = j0 * k;
     for (uint32_t i = tid; i < cnt; i += NT) {
       const uint64_t first = (j0 + i) * k;
-      err |= decode_word<V>(s_words[i], cst, B, (uint32_t)min((uint64_t)k, nb - first), h.y,
-                            s_out + (first - f0));
+      err |= decode_any<V>(s_words[i], cst, h.z, (uint32_t)min((uint64_t)k, nb - first), h.y,
+                           s_out + (first - f0));
     }
     __syncthreads();
     store_values<V>(out + lo + f0, s_out, (uint32_t)(min(nb, j1 * k) - f0));
