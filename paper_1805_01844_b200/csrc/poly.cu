@@ -24,46 +24,59 @@ int g_sms[MAX_DEVICES];
 typedef unsigned __int128 u128;
 
 // Host copies of the tables (exact integer arithmetic).
-uint8_t h_ktab[KTAB_MAX + 1];
+uint16_t h_ktab[KTAB_MAX + 1];
 DecConst h_dtab[KTAB_MAX + 1];
 bool h_tables_built = false;
 
+// k = max{k : B^k <= 2^64}, h = max{h : B^h <= 2^32}; for non-powers of two
+// B^k, R = ceil(2^160 / B^k) and t32 = max{t <= min(k, h) :
+// 2^32 B^k + B^k + 2^64 B^t <= 2^96}.
 void build_tables() {
   if (h_tables_built) return;
   const u128 word_ring = ((u128)1) << 64;
   for (uint64_t B = 0; B <= KTAB_MAX; ++B) {
     DecConst c;
     memset(&c, 0, sizeof c);
-    uint32_t k = 0;
+    uint32_t k = 0, h = 0, log2b = 0, t32 = 0;
     if (B >= 2) {
       u128 p = 1;
       while (p * B <= word_ring) {
         p *= B;
         ++k;
       }
-      c.k = k;
+      u128 q = 1;
+      while (q * B <= (((u128)1) << 32)) {
+        q *= B;
+        ++h;
+      }
       if ((B & (B - 1)) == 0) {
-        uint32_t j = 0;
-        while ((1ull << j) != B) ++j;
-        c.log2b = j;
+        while ((1ull << log2b) != B) ++log2b;
       } else {
         const uint64_t D = (uint64_t)p;  // B^k < 2^64 for non-powers of two
-        u128 rem = 0, q = 0;
+        u128 rem = 0, r = 0;
         for (int i = 160; i >= 0; --i) {
           rem = (rem << 1) | (i == 160 ? 1u : 0u);
-          q <<= 1;
+          r <<= 1;
           if (rem >= D) {
             rem -= D;
-            q |= 1;
+            r |= 1;
           }
         }
-        q += 1;  // ceil: the remainder of 2^160 / D is nonzero
+        r += 1;  // ceil: the remainder of 2^160 / D is nonzero
         c.Bk = D;
-        c.Rl = (uint64_t)q;
-        c.Rh = (uint64_t)(q >> 64);
+        c.Rl = (uint64_t)r;
+        c.Rh = (uint64_t)(r >> 64);
+        const u128 lim96 = ((u128)1) << 96;
+        u128 bt = 1;
+        for (uint32_t t = 1; t <= std::min(k, h); ++t) {
+          bt *= B;
+          if ((((u128)D) << 32) + D + (bt << 64) <= lim96) t32 = t;
+          else break;
+        }
       }
     }
-    h_ktab[B] = (uint8_t)k;
+    c.meta = k | (log2b << 8) | (t32 << 16) | (h << 24);
+    h_ktab[B] = (uint16_t)(k | (h << 8));
     h_dtab[B] = c;
   }
   h_tables_built = true;
@@ -92,7 +105,7 @@ poly_status_t ensure_init(int dev) {
   cudaError_t e = cudaMemcpyToSymbol(g_ktab, h_ktab, sizeof h_ktab);
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_dtab, h_dtab, sizeof h_dtab);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
-  const int wmax = WARPS * (WT_MAX + 512);
+  const int wmax = WARPS * (2 * WT_MAX + 512);
   set_smem_attr(poly_compress_warp<uint16_t, 0>, wmax);
   set_smem_attr(poly_compress_warp<uint16_t, 1>, wmax);
   set_smem_attr(poly_compress_warp<uint32_t, 0>, wmax);
@@ -110,15 +123,6 @@ poly_status_t ensure_init(int dev) {
   if (e != cudaSuccess) return POLY_ERR_CUDA;
   g_ready[dev] = true;
   return POLY_OK;
-}
-
-uint32_t gcd32(uint32_t a, uint32_t b) {
-  while (b) {
-    uint32_t t = a % b;
-    a = b;
-    b = t;
-  }
-  return a;
 }
 
 // Regime and launch shape for (n, w, block_size).  Deterministic: the same
@@ -139,12 +143,15 @@ bool plan(uint64_t n, uint32_t w, uint64_t block_size, Shape& sh, WarpShape& ws,
   if (bb <= WT_MAX) {
     rg = WARP;
     ws.n = n; ws.Le = sh.Le; ws.n_blocks = sh.n_blocks; ws.block_len = sh.block_len; ws.width = w;
+    const uint64_t kmin = w == 16 ? 4 : 2;
     if (bb <= LANE_BLOCK_MAX) {
       ws.mode = 0;
       uint64_t bpl = WT_TARGET / (32 * bb);
-      bpl = std::max<uint64_t>(1, std::min<uint64_t>(4, bpl));
+      bpl = std::max<uint64_t>(1, std::min<uint64_t>(BPL_MAX, bpl));
       ws.WB = (uint32_t)(32 * bpl);
-      ws.slice = (uint32_t)((ws.WB * bb + 15) / 16 * 16);
+      ws.words_off = (uint32_t)((ws.WB * bb + 15) / 16 * 16);
+      ws.words_cap = (uint32_t)(ws.WB * ((sh.Le + kmin - 1) / kmin));
+      ws.slice = ws.words_off + 8 * ws.words_cap;
     } else {
       ws.mode = 1;
       uint64_t wb = WT_TARGET / bb;

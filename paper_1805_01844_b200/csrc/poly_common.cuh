@@ -23,28 +23,44 @@ constexpr uint64_t VAL_MASK = (1ull << 62) - 1;
 constexpr uint32_t CODEC_CONSTANT = 1;
 constexpr uint32_t CODEC_BASIC = 2;
 
-// Per-base decode constants.  For a non-power-of-two
-// base B with capacity k:  Bk = B^k < 2^64 and R = ceil(2^160 / B^k) < 2^128,
-// split R = Rh * 2^64 + Rl.  For B = 2^j the decoder uses shifts instead and
-// only k is meaningful.
+// Per-base constants.  k = max{k : B^k <= 2^64} (Eq. 1,
+// reading R2) and h = max{h : B^h <= 2^32} (32-bit chunk length).  For a
+// non-power-of-two base: Bk = B^k < 2^64 and R = ceil(2^160 / B^k) < 2^128,
+// split R = Rh * 2^64 + Rl; t32 = the number of trailing digits of a word
+// that may be extracted with a 32-bit fraction (Sec. 5.3).  For B = 2^j the
+// decoder uses shifts and only k and log2b are meaningful.
 struct __align__(16) DecConst {
   uint64_t Bk;
   uint64_t Rl;
   uint64_t Rh;
-  uint32_t k;
-  uint32_t log2b;  // j if B = 2^j, else 0
+  uint32_t meta;  // k | log2b << 8 | t32 << 16 | h << 24
+  uint32_t pad;
 };
+__device__ __forceinline__ uint32_t dc_k(const DecConst& c) { return c.meta & 0xffu; }
+__device__ __forceinline__ uint32_t dc_log2b(const DecConst& c) { return (c.meta >> 8) & 0xffu; }
+__device__ __forceinline__ uint32_t dc_t32(const DecConst& c) { return (c.meta >> 16) & 0xffu; }
 
 // Filled once per device by poly_init (host computes them with exact 128-bit
-// integer arithmetic).
-__device__ uint8_t g_ktab[KTAB_MAX + 1];
+// integer arithmetic).  g_ktab[B] = k | h << 8.
+__device__ uint16_t g_ktab[KTAB_MAX + 1];
 __device__ DecConst g_dtab[KTAB_MAX + 1];
 
 // ---------------------------------------------------------------- arithmetic
-// Exact k = max{k : B^k <= 2^64} for B > KTAB_MAX: B^3 <= 2^64 iff B <= 2642245.
+// k and h for any 2 <= B <= 2^32 (B^3 <= 2^64 iff B <= 2642245; B^2 <= 2^32 iff
+// B <= 65536).
 __device__ __forceinline__ uint32_t capacity_of(uint64_t B) {
-  if (B <= KTAB_MAX) return g_ktab[B];
+  if (B <= KTAB_MAX) return g_ktab[B] & 0xffu;
   return B <= 2642245ull ? 3u : 2u;
+}
+__device__ __forceinline__ void capacity_kh(uint64_t B, uint32_t& k, uint32_t& h) {
+  if (B <= KTAB_MAX) {
+    const uint32_t e = g_ktab[B];
+    k = e & 0xffu;
+    h = e >> 8;
+  } else {
+    k = B <= 2642245ull ? 3u : 2u;
+    h = 1u;
+  }
 }
 
 // ceil(2^160 / D) for D not a power of two, D >= 3 (slow path for B > 2^16):
@@ -64,20 +80,28 @@ __device__ __noinline__ void recip160(uint64_t D, uint64_t& Rl, uint64_t& Rh) {
   Rh = (uint64_t)(q >> 64);
 }
 
-__device__ __forceinline__ DecConst dec_const_of(uint64_t B) {
-  if (B <= KTAB_MAX) return g_dtab[B];
+__device__ __noinline__ DecConst dec_const_slow(uint64_t B) {
   DecConst c;
-  c.k = capacity_of(B);
-  c.log2b = ((B & (B - 1)) == 0) ? (uint32_t)(63 - __clzll(B)) : 0u;
-  if (c.log2b) {
-    c.Bk = 0; c.Rl = 0; c.Rh = 0;
-  } else {
+  const uint32_t k = B <= 2642245ull ? 3u : 2u;
+  const uint32_t log2b = ((B & (B - 1)) == 0) ? (uint32_t)(63 - __clzll(B)) : 0u;
+  c.Bk = 0; c.Rl = 0; c.Rh = 0; c.pad = 0;
+  uint32_t t32 = 0;
+  if (!log2b) {
     uint64_t p = 1;
-    for (uint32_t i = 0; i < c.k; ++i) p *= B;
+    for (uint32_t i = 0; i < k; ++i) p *= B;
     c.Bk = p;
     recip160(p, c.Rl, c.Rh);
+    // t32 <= h = 1: one trailing 32-bit digit iff 2^32 B^k + B^k + 2^64 B <= 2^96
+    const unsigned __int128 lhs = ((unsigned __int128)p << 32) + p + ((unsigned __int128)B << 64);
+    if (lhs <= ((unsigned __int128)1 << 96)) t32 = 1;
   }
+  c.meta = k | (log2b << 8) | (t32 << 16) | (1u << 24);
   return c;
+}
+
+__device__ __forceinline__ DecConst dec_const_of(uint64_t B) {
+  if (B <= KTAB_MAX) return g_dtab[B];
+  return dec_const_slow(B);
 }
 
 // ---------------------------------------------------------------- memory
@@ -161,26 +185,30 @@ __device__ T cta_exclusive_scan(const T* in, T* out, uint32_t count, T* s_warp) 
 // exclusive prefix of the tile (same value in every lane).  Tiles are handed
 // out in order by an atomic ticket, so every predecessor is resident or done
 // and the spin terminates.
+// Lane l inspects tile (base - l); the window resolves as soon as the nearest
+// published inclusive prefix is closer than the nearest unpublished tile, so
+// a slow tile further back never delays its successors.  Unresolved windows
+// are re-read with a growing back-off to keep the spin off the L2.
 __device__ __forceinline__ uint64_t lookback(const uint64_t* status, uint64_t tile) {
   const int lane = threadIdx.x & 31;
   uint64_t excl = 0;
   int64_t base = (int64_t)tile - 1;
+  uint32_t ns = 0;
   while (true) {
     const int64_t idx = base - lane;
-    uint64_t st = FLAG_PRE;  // before tile 0: prefix 0
-    if (idx >= 0) {
-      do {
-        st = ld_relaxed_u64(status + idx);
-      } while ((st >> 62) == 0);
-    }
+    const uint64_t st = idx >= 0 ? ld_relaxed_u64(status + idx) : FLAG_PRE;  // before tile 0: 0
     const uint32_t pre = __ballot_sync(0xffffffffu, (st & FLAG_PRE) != 0);
-    uint64_t v = st & VAL_MASK;
-    if (pre) {
+    const uint32_t inval = __ballot_sync(0xffffffffu, (st >> 62) == 0);
+    if (pre && (inval == 0 || __ffs(pre) < __ffs(inval))) {
       const int first = __ffs(pre) - 1;
-      if (lane > first) v = 0;
-      return excl + warp_sum_u64(v);
+      return excl + warp_sum_u64(lane <= first ? (st & VAL_MASK) : 0ull);
     }
-    excl += warp_sum_u64(v);
+    if (inval) {
+      if (ns) __nanosleep(ns);
+      ns = ns ? min(ns * 2, 1024u) : 32u;
+      continue;
+    }
+    excl += warp_sum_u64(st & VAL_MASK);
     base -= 32;
   }
 }

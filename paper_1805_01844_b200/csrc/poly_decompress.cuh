@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(NT) poly_decompress_unpack(DecompressArgs a) {
     if (tid == 0) s_c = dec_const_of(B);
     __syncthreads();
     const DecConst cst = s_c;
-    const uint32_t k = cst.k;
+    const uint32_t k = dc_k(cst);
     if (check_block(h, nb, sh.width, k)) continue;
     const uint64_t nw = h.w;
     const uint64_t j0 = (c * CH_VALUES + k - 1) / k;

@@ -1,18 +1,20 @@
-// poly_warp.cuh -- warp-tile kernels (blocks of up to WT_MAX bytes).
+// poly_warp.cuh -- warp-tile kernels (blocks of up to WT_MAX bytes) and the
+// word codec shared with the large-block kernels.
 //
-// Each warp owns one look-back unit: a run of consecutive blocks of the
-// stream, handed out in order by an atomic ticket.  No CTA barrier is used:
-// a warp stages its unit in its own shared-memory slice, computes the
-// per-block statistics, scans its word counts with shuffles, publishes its
-// aggregate, looks back for its payload offset, then writes headers and
-// words straight to global memory (coalesced 8-byte word stores in the
-// lanes-per-block mode, 16-byte header stores).
+// Each warp owns one look-back unit at a time: a run of consecutive blocks
+// of the stream, handed out in order by an atomic ticket (persistent grid).
+// No CTA barrier is used.  A warp stages its unit in its own shared-memory
+// slice, computes the per-block statistics, scans the word counts with
+// shuffles, publishes its aggregate, looks back for its payload offset and
+// writes headers and words with coalesced stores.
 //
 // Two mappings (chosen on the host, see poly.cu plan()):
-//   MODE_LANE  (block <= 128 B, e.g. cfg2's 30 x u16): lane l owns blocks
-//              l, l+32, ... of the unit (BPL blocks per lane).
-//   MODE_WARP  (128 B < block <= WT_MAX): the 32 lanes cooperate on each
-//              block; WB blocks per unit; lane l owns words l, l+32, ...
+//   MODE 0 (block <= 128 B, e.g. cfg2's 30 x u16): lane l owns blocks
+//          l, l+32, ... of the unit (BPL blocks per lane).  Words are staged
+//          in smem before the look-back, so the look-back latency overlaps the
+//          packing and the payload leaves with contiguous 8-byte stores.
+//   MODE 1 (128 B < block <= WT_MAX): the 32 lanes cooperate on each block
+//          (WB blocks per unit); lane l owns words l, l+32, ... (contiguous).
 #pragma once
 #include "poly_common.cuh"
 
@@ -21,13 +23,16 @@ namespace polyk {
 constexpr int WARPS = 4;               // warps per CTA (independent)
 constexpr uint32_t WT_MAX = 8192;      // bytes of input per warp unit
 constexpr uint32_t LANE_BLOCK_MAX = 128;
+constexpr int BPL_MAX = 4;             // MODE 0: blocks per lane
 
 struct WarpShape {
   uint64_t n, Le, n_blocks;
   uint32_t block_len, width;
-  uint32_t WB;        // blocks per unit
-  uint32_t mode;      // 0 lane, 1 warp
-  uint32_t slice;     // smem bytes per warp (16-aligned)
+  uint32_t WB;         // blocks per unit
+  uint32_t mode;       // 0 lane, 1 warp
+  uint32_t slice;      // smem bytes per warp (16-aligned)
+  uint32_t words_off;  // MODE 0: byte offset of the word area in the slice
+  uint32_t words_cap;  // MODE 0: capacity of the word area (words)
   uint64_t n_units;
 };
 
@@ -42,42 +47,50 @@ struct WarpArgs {
   WarpShape sh;
 };
 
+// ------------------------------------------------------------------ helpers
 __device__ __forceinline__ uint32_t warp_ticket(uint32_t* ticket) {
   uint32_t t = 0;
   if ((threadIdx.x & 31) == 0) t = atomicAdd(ticket, 1u);
   return __shfl_sync(0xffffffffu, t, 0);
 }
 
-// Look-back for a warp unit: publish the aggregate, fetch the exclusive
-// prefix, publish the inclusive prefix.  All lanes return the prefix.
-__device__ __forceinline__ uint64_t warp_publish_and_lookback(uint64_t* status, uint64_t unit,
-                                                             uint64_t total) {
-  const int lane = threadIdx.x & 31;
-  if (unit == 0) {
-    if (lane == 0) st_relaxed_u64(status, FLAG_PRE | (total & VAL_MASK));
-    return 0;
-  }
-  if (lane == 0) st_relaxed_u64(status + unit, FLAG_AGG | (total & VAL_MASK));
+__device__ __forceinline__ void warp_publish_agg(uint64_t* status, uint64_t unit, uint64_t total) {
+  if ((threadIdx.x & 31) == 0)
+    st_relaxed_u64(status + unit, (unit == 0 ? FLAG_PRE : FLAG_AGG) | (total & VAL_MASK));
+}
+
+// Exclusive prefix of `unit`, then publish its inclusive prefix.
+__device__ __forceinline__ uint64_t warp_lookback(uint64_t* status, uint64_t unit, uint64_t total) {
+  if (unit == 0) return 0;
   const uint64_t p = lookback(status, unit);
-  if (lane == 0) st_relaxed_u64(status + unit, FLAG_PRE | ((p + total) & VAL_MASK));
+  if ((threadIdx.x & 31) == 0) st_relaxed_u64(status + unit, FLAG_PRE | ((p + total) & VAL_MASK));
   return p;
 }
 
+// ceil(n / k) for n < 2^24, 1 <= k <= 64, without an integer divide.
+__device__ __forceinline__ uint32_t ceil_div_small(uint32_t n, uint32_t k) {
+  uint32_t q = (uint32_t)__fmul_rz((float)(n + k - 1), __frcp_rn((float)k));
+  if (q * k > n + k - 1) --q;
+  if ((q + 1) * k <= n + k - 1) ++q;
+  return q;
+}
+
 // Copy nbytes from global g to this warp's smem slice s (16-byte vectors when
-// both are aligned, bytes otherwise).  Caller issues __syncwarp() after.
+// g is 16-byte aligned; bytes otherwise).  Up to 8 loads in flight per lane.
 __device__ __forceinline__ void warp_copy_in(uint8_t* s, const uint8_t* g, uint32_t nbytes) {
   const int lane = threadIdx.x & 31;
   uint32_t done = 0;
-  const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(g) & 15);
-  if (mis == 0) {
+  if ((reinterpret_cast<uintptr_t>(g) & 15) == 0) {
     const uint32_t n16 = nbytes >> 4;
     const uint4* gv = reinterpret_cast<const uint4*>(g);
     uint4* sv = reinterpret_cast<uint4*>(s);
     uint32_t i = lane;
-    for (; i + 96 < n16; i += 128) {
-      const uint4 a = ldg_nc_v4(gv + i), b = ldg_nc_v4(gv + i + 32), c = ldg_nc_v4(gv + i + 64),
-                  d = ldg_nc_v4(gv + i + 96);
-      sv[i] = a; sv[i + 32] = b; sv[i + 64] = c; sv[i + 96] = d;
+    for (; i + 7 * 32 < n16; i += 8 * 32) {
+      uint4 r[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) r[q] = ldg_nc_v4(gv + i + 32 * q);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) sv[i + 32 * q] = r[q];
     }
     for (; i < n16; i += 32) sv[i] = ldg_nc_v4(gv + i);
     done = n16 << 4;
@@ -85,6 +98,7 @@ __device__ __forceinline__ void warp_copy_in(uint8_t* s, const uint8_t* g, uint3
   for (uint32_t i = done + lane; i < nbytes; i += 32) s[i] = g[i];
 }
 
+// Copy nbytes from smem s to global g (16-byte stores when g is aligned).
 __device__ __forceinline__ void warp_copy_out(uint8_t* g, const uint8_t* s, uint32_t nbytes) {
   const int lane = threadIdx.x & 31;
   uint32_t done = 0;
@@ -97,20 +111,37 @@ __device__ __forceinline__ void warp_copy_out(uint8_t* g, const uint8_t* s, uint
   for (uint32_t i = done + lane; i < nbytes; i += 32) g[i] = s[i];
 }
 
-// min / max of n values at s (any alignment of the block start within smem)
+// Copy `cnt` u64 words between global (8-byte aligned) and smem, coalesced.
+__device__ __forceinline__ void warp_words_in(uint64_t* s, const uint64_t* g, uint32_t cnt) {
+  const int lane = threadIdx.x & 31;
+  uint32_t i = lane;
+  for (; i + 3 * 32 < cnt; i += 4 * 32) {
+    uint64_t r[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) r[q] = ldg_nc_u64(g + i + 32 * q);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) s[i + 32 * q] = r[q];
+  }
+  for (; i < cnt; i += 32) s[i] = ldg_nc_u64(g + i);
+}
+
+// min / max of n values at s.
 template <typename V>
 __device__ __forceinline__ void block_minmax(const V* s, uint32_t n, uint32_t& mn, uint32_t& mx) {
-  mn = 0xffffffffu;
-  mx = 0u;
-  if (sizeof(V) == 2 && (reinterpret_cast<uintptr_t>(s) & 3) == 0) {
+  if (sizeof(V) == 2 && (reinterpret_cast<uintptr_t>(s) & 3) == 0 && n >= 2) {
     const uint32_t* w = reinterpret_cast<const uint32_t*>(s);
-    uint32_t a = 0xffffffffu, b = 0u;
     const uint32_t nw = n >> 1;
+    uint32_t a = w[0], b = w[0];
+    uint32_t i = 1;
 #pragma unroll 4
-    for (uint32_t i = 0; i < nw; ++i) {
-      const uint32_t x = w[i];
-      a = __vminu2(a, x);
-      b = __vmaxu2(b, x);
+    for (; i + 1 < nw; i += 2) {
+      const uint32_t x = w[i], y = w[i + 1];
+      a = __vimin3_u16x2(a, x, y);
+      b = __vimax3_u16x2(b, x, y);
+    }
+    if (i < nw) {
+      a = __vminu2(a, w[i]);
+      b = __vmaxu2(b, w[i]);
     }
     mn = min(a & 0xffffu, a >> 16);
     mx = max(b & 0xffffu, b >> 16);
@@ -119,8 +150,9 @@ __device__ __forceinline__ void block_minmax(const V* s, uint32_t n, uint32_t& m
       mn = min(mn, x);
       mx = max(mx, x);
     }
-    if (nw == 0 && !(n & 1)) { mn = 0xffffffffu; mx = 0; }
   } else {
+    mn = 0xffffffffu;
+    mx = 0u;
 #pragma unroll 4
     for (uint32_t i = 0; i < n; ++i) {
       const uint32_t x = (uint32_t)s[i];
@@ -130,25 +162,149 @@ __device__ __forceinline__ void block_minmax(const V* s, uint32_t n, uint32_t& m
   }
 }
 
+// ------------------------------------------------------------------ pack (a5)
+// Horner of Eq. 2 over 32-bit chunks of h digits:
+// s = sum_q c_q D^q, D = B^h, each chunk c_q < B^h <= 2^32 evaluated with
+// 32-bit multiply-adds, chunks combined top-down with 64x32 multiply-adds.
+// Requires B <= 2^32 - 1 (B = 2^32 goes through pack_word_b32).
 template <typename V>
-__device__ __forceinline__ uint64_t horner(const V* v, uint32_t m, uint32_t B, uint32_t vmin) {
-  uint64_t s = 0;
+__device__ __forceinline__ uint32_t chunk32(const V* v, uint32_t len, uint32_t B, uint32_t vmin) {
+  uint32_t c = 0;
 #pragma unroll 4
-  for (int i = (int)m - 1; i >= 0; --i) s = s * B + (uint32_t)((uint32_t)v[i] - vmin);
+  for (int i = (int)len - 1; i >= 0; --i) c = c * B + ((uint32_t)v[i] - vmin);
+  return c;
+}
+
+template <typename V>
+__device__ __forceinline__ uint64_t pack_word(const V* v, uint32_t m, uint32_t B, uint32_t h, uint32_t D,
+                                              uint32_t vmin) {
+  // chunks from the top: the top one holds r = m - (nch-1) h digits
+  const uint32_t nch = m <= h ? 1u : (m <= 2 * h ? 2u : 3u);
+  const uint32_t r = m - (nch - 1) * h;
+  uint64_t s = chunk32<V>(v + (nch - 1) * h, r, B, vmin);
+  for (int q = (int)nch - 2; q >= 0; --q) {
+    const uint32_t c = chunk32<V>(v + q * h, h, B, vmin);
+    if (D == 0)  // D = 2^32 (B = 2^j, j | 32)
+      s = (s << 32) | c;
+    else
+      s = s * D + c;
+  }
   return s;
 }
 
-// Horner for B = 2^32 (only u32 data with v_min = 0 and v_max = 2^32-1).
 template <typename V>
-__device__ __forceinline__ uint64_t horner_b32(const V* v, uint32_t m, uint32_t vmin) {
+__device__ __forceinline__ uint64_t pack_word_b32(const V* v, uint32_t m, uint32_t vmin) {
   uint64_t s = 0;
   for (int i = (int)m - 1; i >= 0; --i) s = (s << 32) | (uint32_t)((uint32_t)v[i] - vmin);
   return s;
 }
 
+// Per-block packing parameters.
+struct PackParams {
+  uint32_t B, h, D, k;
+};
+__device__ __forceinline__ PackParams pack_params(uint32_t bm1) {
+  PackParams p;
+  p.B = bm1 + 1;  // wraps to 0 for B = 2^32 (handled by pack_word_b32)
+  capacity_kh((uint64_t)bm1 + 1, p.k, p.h);
+  uint64_t D = 1;
+  for (uint32_t i = 0; i < p.h; ++i) D *= (uint64_t)bm1 + 1;
+  p.D = (uint32_t)D;  // 0 iff D = 2^32
+  return p;
+}
+
+template <typename V>
+__device__ __forceinline__ uint64_t pack_any(const V* v, uint32_t m, const PackParams& p, uint32_t vmin) {
+  if (p.B == 0) return pack_word_b32<V>(v, m, vmin);
+  return pack_word<V>(v, m, p.B, p.h, p.D, vmin);
+}
+
+// ------------------------------------------------------------------ unpack (a8)
+// Word -> digits, most significant first, through the binary fraction
+// f in [s 2^64 / B^k, (s+1) 2^64 / B^k):
+//   f = floor(s R / 2^96) + 1,  R = ceil(2^160 / B^k);
+//   64-bit step: (d, f) = (floor(f B / 2^64), f B mod 2^64);
+//   after k - t32 digits the top 32 bits + 1 are an exact 32-bit fraction for
+//   the last t32 digits: (d, g) = (floor(g B / 2^32), g B mod 2^32).
+template <typename V>
+__device__ __forceinline__ uint32_t decode_frac(uint64_t s, const DecConst& c, uint32_t B, uint32_t m,
+                                                uint32_t vmin, V* out) {
+  if (s >= c.Bk) return POLY_ST_RESIDUE;
+  const uint64_t hi1 = __umul64hi(s, c.Rl);
+  const uint64_t lo2 = s * c.Rh;
+  const uint64_t hi2 = __umul64hi(s, c.Rh);
+  const uint64_t mid = lo2 + hi1;
+  const uint64_t f = ((hi2 + (mid < lo2 ? 1ull : 0ull)) << 32) + (mid >> 32) + 1;
+  uint32_t f0 = (uint32_t)f, f1 = (uint32_t)(f >> 32);
+  const int k = (int)dc_k(c), t = (int)dc_t32(c), mm = (int)m;
+  uint32_t extra = 0;
+  int i = k - 1;
+  const int za = max(t, mm);
+  for (; i >= za; --i) {  // 64-bit steps, digits that must be zero
+    const uint64_t t0 = (uint64_t)f0 * B;
+    const uint64_t t1 = (uint64_t)f1 * B + (uint32_t)(t0 >> 32);
+    extra |= (uint32_t)(t1 >> 32);
+    f1 = (uint32_t)t1;
+    f0 = (uint32_t)t0;
+  }
+#pragma unroll 2
+  for (; i >= t; --i) {  // 64-bit steps, output digits
+    const uint64_t t0 = (uint64_t)f0 * B;
+    const uint64_t t1 = (uint64_t)f1 * B + (uint32_t)(t0 >> 32);
+    out[i] = (V)(vmin + (uint32_t)(t1 >> 32));
+    f1 = (uint32_t)t1;
+    f0 = (uint32_t)t0;
+  }
+  uint32_t g = f1 + 1;
+  for (; i >= mm; --i) {  // 32-bit steps, digits that must be zero
+    const uint64_t p = (uint64_t)g * B;
+    extra |= (uint32_t)(p >> 32);
+    g = (uint32_t)p;
+  }
+#pragma unroll 4
+  for (; i >= 0; --i) {  // 32-bit steps, output digits
+    const uint64_t p = (uint64_t)g * B;
+    out[i] = (V)(vmin + (uint32_t)(p >> 32));
+    g = (uint32_t)p;
+  }
+  return extra ? POLY_ST_RESIDUE : 0u;
+}
+
+template <typename V>
+__device__ __forceinline__ uint32_t decode_pow2(uint64_t s, uint32_t j, uint32_t m, uint32_t vmin, V* out) {
+  const uint64_t mask = (1ull << j) - 1;  // j <= 32
+#pragma unroll 4
+  for (uint32_t i = 0; i < m; ++i) out[i] = (V)(vmin + (uint32_t)((s >> (i * j)) & mask));
+  return (m * j < 64 && (s >> (m * j)) != 0) ? POLY_ST_RESIDUE : 0u;
+}
+
+template <typename V>
+__device__ __forceinline__ uint32_t decode_any(uint64_t s, const DecConst& c, uint32_t bm1, uint32_t m,
+                                               uint32_t vmin, V* out) {
+  const uint32_t j = dc_log2b(c);
+  if (j) return decode_pow2<V>(s, j, m, vmin, out);
+  return decode_frac<V>(s, c, bm1 + 1, m, vmin, out);
+}
+
+// Block-header validation (a9) without an integer divide: n_words must be
+// ceil(n_b / k), i.e. (n_words - 1) k < n_b <= n_words k.
+__device__ __forceinline__ uint32_t check_block_hdr(uint4 h, uint32_t nb, uint32_t width, uint32_t k) {
+  const uint64_t vmax_allowed = (width == 16) ? 0xffffull : 0xffffffffull;
+  if (h.x == CODEC_CONSTANT) {
+    uint32_t e = 0;
+    if (h.z != 0 || h.w != 0) e |= POLY_ST_NWORDS;
+    if ((uint64_t)h.y > vmax_allowed) e |= POLY_ST_OVERFLOW;
+    return e;
+  }
+  if (h.x != CODEC_BASIC) return POLY_ST_BAD_CODEC;
+  if (h.z == 0 || (uint64_t)h.y + h.z > vmax_allowed) return POLY_ST_OVERFLOW;
+  if (h.w == 0 || (uint64_t)(h.w - 1) * k >= nb || (uint64_t)h.w * k < nb) return POLY_ST_NWORDS;
+  return 0;
+}
+
 __device__ __forceinline__ void write_global_header_w(uint8_t* out, const WarpShape& sh, uint64_t pw) {
   uint4 h0, h1;
-  h0.x = 0x43594c50u;
+  h0.x = 0x43594c50u;  // "PLYC"
   h0.y = 2u | (sh.width << 16);
   h0.z = (uint32_t)sh.n;
   h0.w = (uint32_t)(sh.n >> 32);
@@ -158,6 +314,17 @@ __device__ __forceinline__ void write_global_header_w(uint8_t* out, const WarpSh
   h1.w = (uint32_t)((pw * 8) >> 32);
   reinterpret_cast<uint4*>(out)[0] = h0;
   reinterpret_cast<uint4*>(out)[1] = h1;
+}
+
+// inclusive warp scan
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
 }
 
 // ======================================================================
@@ -186,64 +353,59 @@ __global__ void __launch_bounds__(WARPS * 32) poly_compress_warp(WarpArgs a) {
 
     if (MODE == 0) {
       // ---------------- lane per block
-      constexpr int BPL_MAX = 4;
-      uint32_t vmin[BPL_MAX], Bv[BPL_MAX], nw[BPL_MAX], off[BPL_MAX];
+      uint64_t* sw = reinterpret_cast<uint64_t*>(slice + sh.words_off);
+      uint32_t vmin[BPL_MAX], bm1[BPL_MAX], nw[BPL_MAX], off[BPL_MAX];
       uint32_t carry = 0;
+      const int rounds = (int)((nblk + 31) >> 5);
 #pragma unroll
       for (int r = 0; r < BPL_MAX; ++r) {
-        const uint32_t lb = r * 32 + lane;
-        uint32_t w = 0, mn = 0, mx = 0;
-        if (lb < nblk) {
-          const uint32_t nb = min(L, nv - lb * L);
-          block_minmax<V>(sv + lb * L, nb, mn, mx);
-          const uint64_t B = (uint64_t)mx - mn + 1;
-          if (B > 1) {
-            const uint32_t k = capacity_of(B);
-            w = (nb + k - 1) / k;
-          }
-        }
-        vmin[r] = mn;
-        Bv[r] = mx - mn;  // B - 1
-        nw[r] = w;
-        // inclusive warp scan of w
-        uint32_t x = w;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-          if (lane >= o) x += y;
-        }
-        off[r] = carry + x - w;
-        carry += __shfl_sync(0xffffffffu, x, 31);
-        if ((r + 1) * 32 >= (int)nblk) break;
-      }
-      const uint64_t P = warp_publish_and_lookback(a.status, unit, carry);
-#pragma unroll
-      for (int r = 0; r < BPL_MAX; ++r) {
-        const uint32_t lb = r * 32 + lane;
-        if (lb < nblk) {
-          const uint32_t bm1 = Bv[r];
-          hdr_out[b0 + lb] = make_uint4(bm1 == 0 ? CODEC_CONSTANT : CODEC_BASIC, vmin[r], bm1, nw[r]);
-          if (bm1 != 0) {
+        vmin[r] = 0; bm1[r] = 0; nw[r] = 0; off[r] = 0;
+        if (r < rounds) {
+          const uint32_t lb = r * 32 + lane;
+          if (lb < nblk) {
             const uint32_t nb = min(L, nv - lb * L);
-            const uint64_t B = (uint64_t)bm1 + 1;
-            const uint32_t k = capacity_of(B);
-            uint64_t* dst = pay + P + off[r];
-            const V* src = sv + lb * L;
-            for (uint32_t j = 0; j < nw[r]; ++j) {
-              const uint32_t first = j * k, m = min(k, nb - first);
-              dst[j] = (bm1 == 0xffffffffu) ? horner_b32<V>(src + first, m, vmin[r])
-                                            : horner<V>(src + first, m, bm1 + 1, vmin[r]);
-            }
+            uint32_t mn, mx;
+            block_minmax<V>(sv + lb * L, nb, mn, mx);
+            vmin[r] = mn;
+            bm1[r] = mx - mn;
+            if (mx != mn) nw[r] = ceil_div_small(nb, capacity_of((uint64_t)(mx - mn) + 1));
           }
+          const uint32_t x = warp_incl_scan(nw[r]);
+          off[r] = carry + x - nw[r];
+          carry += __shfl_sync(0xffffffffu, x, 31);
         }
-        if ((r + 1) * 32 >= (int)nblk) break;
       }
+      warp_publish_agg(a.status, unit, carry);
+      // pack into the word area (overlaps the predecessors' progress)
+#pragma unroll
+      for (int r = 0; r < BPL_MAX; ++r) {
+        const uint32_t lb = r * 32 + lane;
+        if (r < rounds && lb < nblk && bm1[r] != 0) {
+          const uint32_t nb = min(L, nv - lb * L);
+          const PackParams pp = pack_params(bm1[r]);
+          const V* src = sv + lb * L;
+          uint64_t* dst = sw + off[r];
+          for (uint32_t j = 0, first = 0; j < nw[r]; ++j, first += pp.k)
+            dst[j] = pack_any<V>(src + first, min(pp.k, nb - first), pp, vmin[r]);
+        }
+      }
+      const uint64_t P = warp_lookback(a.status, unit, carry);
+#pragma unroll
+      for (int r = 0; r < BPL_MAX; ++r) {
+        const uint32_t lb = r * 32 + lane;
+        if (r < rounds && lb < nblk)
+          hdr_out[b0 + lb] = make_uint4(bm1[r] == 0 ? CODEC_CONSTANT : CODEC_BASIC, vmin[r], bm1[r], nw[r]);
+      }
+      __syncwarp();
+      uint64_t* dst = pay + P;
+      for (uint32_t i = lane; i < carry; i += 32) dst[i] = sw[i];
       if (unit == sh.n_units - 1 && lane == 0) {
         write_global_header_w(a.out, sh, P + carry);
         *a.compressed_bytes = 32 + 16 * sh.n_blocks + 8 * (P + carry);
       }
     } else {
       // ---------------- warp per block
+      uint32_t* st = reinterpret_cast<uint32_t*>(slice + sh.slice - 16 * 32);
       uint64_t total = 0;
       for (uint32_t lb = 0; lb < nblk; ++lb) {
         const uint32_t nb = min(L, nv - lb * L);
@@ -251,16 +413,17 @@ __global__ void __launch_bounds__(WARPS * 32) poly_compress_warp(WarpArgs a) {
         uint32_t mn = 0xffffffffu, mx = 0;
         if (sizeof(V) == 2 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
           const uint4* q = reinterpret_cast<const uint4*>(src);
-          uint32_t a0 = 0xffffffffu, b0v = 0;
+          uint32_t a0 = 0xffffffffu, a1 = 0u;
           const uint32_t n8 = nb >> 3;
           for (uint32_t i = lane; i < n8; i += 32) {
             const uint4 t = q[i];
-            a0 = __vminu2(__vminu2(a0, t.x), __vminu2(t.y, __vminu2(t.z, t.w)));
-            b0v = __vmaxu2(__vmaxu2(b0v, t.x), __vmaxu2(t.y, __vmaxu2(t.z, t.w)));
+            a0 = __vimin3_u16x2(a0, t.x, t.y);
+            a0 = __vimin3_u16x2(a0, t.z, t.w);
+            a1 = __vimax3_u16x2(a1, t.x, t.y);
+            a1 = __vimax3_u16x2(a1, t.z, t.w);
           }
           mn = min(a0 & 0xffffu, a0 >> 16);
-          mx = max(b0v & 0xffffu, b0v >> 16);
-          if (n8 == 0) { mn = 0xffffffffu; mx = 0; }
+          mx = max(a1 & 0xffffu, a1 >> 16);
           for (uint32_t i = (n8 << 3) + lane; i < nb; i += 32) {
             mn = min(mn, (uint32_t)src[i]);
             mx = max(mx, (uint32_t)src[i]);
@@ -273,32 +436,33 @@ __global__ void __launch_bounds__(WARPS * 32) poly_compress_warp(WarpArgs a) {
         }
         mn = shfl_min(mn, 32);
         mx = shfl_max(mx, 32);
-        const uint64_t B = (uint64_t)mx - mn + 1;
-        const uint32_t w = B == 1 ? 0u : (nb + capacity_of(B) - 1) / capacity_of(B);
-        // per-block stats go to the 512-byte scratch at the end of the slice
-        uint32_t* st = reinterpret_cast<uint32_t*>(slice + sh.slice - 16 * 32);
-        if (lane == 0) { st[4 * lb] = mn; st[4 * lb + 1] = mx - mn; st[4 * lb + 2] = w; st[4 * lb + 3] = (uint32_t)total; }
+        const uint32_t w = mx == mn ? 0u : ceil_div_small(nb, capacity_of((uint64_t)(mx - mn) + 1));
+        if (lane == 0) {
+          st[4 * lb] = mn;
+          st[4 * lb + 1] = mx - mn;
+          st[4 * lb + 2] = w;
+          st[4 * lb + 3] = (uint32_t)total;
+        }
         total += w;
       }
+      warp_publish_agg(a.status, unit, total);
       __syncwarp();
-      const uint64_t P = warp_publish_and_lookback(a.status, unit, total);
-      const uint32_t* st = reinterpret_cast<const uint32_t*>(slice + sh.slice - 16 * 32);
       if (lane < (int)nblk) {
         const uint32_t bm1 = st[4 * lane + 1];
         hdr_out[b0 + lane] = make_uint4(bm1 == 0 ? CODEC_CONSTANT : CODEC_BASIC, st[4 * lane], bm1,
                                         st[4 * lane + 2]);
       }
+      const uint64_t P = warp_lookback(a.status, unit, total);
       for (uint32_t lb = 0; lb < nblk; ++lb) {
         const uint32_t vmin = st[4 * lb], bm1 = st[4 * lb + 1], w = st[4 * lb + 2];
         if (bm1 == 0) continue;
         const uint32_t nb = min(L, nv - lb * L);
-        const uint32_t k = capacity_of((uint64_t)bm1 + 1);
+        const PackParams pp = pack_params(bm1);
         const V* src = sv + lb * L;
         uint64_t* dst = pay + P + st[4 * lb + 3];
         for (uint32_t j = lane; j < w; j += 32) {
-          const uint32_t first = j * k, m = min(k, nb - first);
-          dst[j] = (bm1 == 0xffffffffu) ? horner_b32<V>(src + first, m, vmin)
-                                        : horner<V>(src + first, m, bm1 + 1, vmin);
+          const uint32_t first = j * pp.k;
+          dst[j] = pack_any<V>(src + first, min(pp.k, nb - first), pp, vmin);
         }
       }
       if (unit == sh.n_units - 1 && lane == 0) {
@@ -313,53 +477,6 @@ __global__ void __launch_bounds__(WARPS * 32) poly_compress_warp(WarpArgs a) {
 // ======================================================================
 // decompress
 // ======================================================================
-// Word -> digits, most significant first, via the 64-bit fraction
-// f in [s 2^64 / B^k, (s+1) 2^64 / B^k).
-template <typename V>
-__device__ __forceinline__ uint32_t decode_frac(uint64_t s, const DecConst& c, uint32_t B, uint32_t m,
-                                                uint32_t vmin, V* out) {
-  if (s >= c.Bk) return POLY_ST_RESIDUE;
-  const uint64_t hi1 = __umul64hi(s, c.Rl);
-  const uint64_t lo2 = s * c.Rh;
-  const uint64_t hi2 = __umul64hi(s, c.Rh);
-  const uint64_t mid = lo2 + hi1;
-  const uint64_t f = ((hi2 + (mid < lo2 ? 1ull : 0ull)) << 32) + (mid >> 32) + 1;
-  uint32_t f0 = (uint32_t)f, f1 = (uint32_t)(f >> 32);
-  uint32_t extra = 0;
-  int i = (int)c.k - 1;
-  for (; i >= (int)m; --i) {
-    const uint64_t t0 = (uint64_t)f0 * B;
-    const uint64_t t1 = (uint64_t)f1 * B + (t0 >> 32);
-    extra |= (uint32_t)(t1 >> 32);
-    f1 = (uint32_t)t1;
-    f0 = (uint32_t)t0;
-  }
-#pragma unroll 4
-  for (; i >= 0; --i) {
-    const uint64_t t0 = (uint64_t)f0 * B;
-    const uint64_t t1 = (uint64_t)f1 * B + (t0 >> 32);
-    out[i] = (V)(vmin + (uint32_t)(t1 >> 32));
-    f1 = (uint32_t)t1;
-    f0 = (uint32_t)t0;
-  }
-  return extra ? POLY_ST_RESIDUE : 0u;
-}
-
-template <typename V>
-__device__ __forceinline__ uint32_t decode_pow2(uint64_t s, uint32_t j, uint32_t m, uint32_t vmin, V* out) {
-  const uint64_t mask = (j >= 64) ? ~0ull : ((1ull << j) - 1);
-#pragma unroll 4
-  for (uint32_t i = 0; i < m; ++i) out[i] = (V)(vmin + (uint32_t)((s >> (i * j)) & mask));
-  return (m * j < 64 && (s >> (m * j)) != 0) ? POLY_ST_RESIDUE : 0u;
-}
-
-template <typename V>
-__device__ __forceinline__ uint32_t decode_any(uint64_t s, const DecConst& c, uint32_t bm1, uint32_t m,
-                                               uint32_t vmin, V* out) {
-  if (c.log2b) return decode_pow2<V>(s, c.log2b, m, vmin, out);
-  return decode_frac<V>(s, c, bm1 + 1, m, vmin, out);
-}
-
 // Global-header check by lane 0, broadcast.  Returns status bits.
 __device__ __forceinline__ uint32_t warp_check_header(const WarpArgs& a, uint64_t* pw) {
   uint32_t e = 0;
@@ -385,20 +502,6 @@ __device__ __forceinline__ uint32_t warp_check_header(const WarpArgs& a, uint64_
   }
   *pw = __shfl_sync(0xffffffffu, p, 0);
   return __shfl_sync(0xffffffffu, e, 0);
-}
-
-__device__ __forceinline__ uint32_t check_block_hdr(uint4 h, uint32_t nb, uint32_t width, uint32_t k) {
-  const uint64_t vmax_allowed = (width == 16) ? 0xffffull : 0xffffffffull;
-  if (h.x == CODEC_CONSTANT) {
-    uint32_t e = 0;
-    if (h.z != 0 || h.w != 0) e |= POLY_ST_NWORDS;
-    if ((uint64_t)h.y > vmax_allowed) e |= POLY_ST_OVERFLOW;
-    return e;
-  }
-  if (h.x != CODEC_BASIC) return POLY_ST_BAD_CODEC;
-  if (h.z == 0 || (uint64_t)h.y + h.z > vmax_allowed) return POLY_ST_OVERFLOW;
-  if (h.w != (nb + k - 1) / k) return POLY_ST_NWORDS;
-  return 0;
 }
 
 template <typename V, int MODE>
@@ -428,62 +531,63 @@ __global__ void __launch_bounds__(WARPS * 32) poly_decompress_warp(WarpArgs a) {
     const uint32_t nv = (uint32_t)(min(sh.n, v0 + (uint64_t)sh.WB * sh.Le) - v0);
 
     if (MODE == 0) {
-      constexpr int BPL_MAX = 4;
+      uint64_t* sw = reinterpret_cast<uint64_t*>(slice + sh.words_off);
       uint4 h[BPL_MAX];
-      uint32_t off[BPL_MAX], ok[BPL_MAX];
-      uint64_t carry = 0;
+      uint32_t off[BPL_MAX];
+      uint32_t carry = 0;
+      const int rounds = (int)((nblk + 31) >> 5);
 #pragma unroll
       for (int r = 0; r < BPL_MAX; ++r) {
         const uint32_t lb = r * 32 + lane;
-        uint32_t w = 0;
-        ok[r] = 0;
         h[r] = make_uint4(0, 0, 0, 0);
-        if (lb < nblk) {
-          h[r] = hdr[b0 + lb];
-          const uint32_t nb = min(L, nv - lb * L);
-          const uint32_t k = (h[r].x == CODEC_BASIC && h[r].z != 0) ? capacity_of((uint64_t)h[r].z + 1) : 1u;
-          const uint32_t e = check_block_hdr(h[r], nb, sh.width, k);
-          err |= e;
-          ok[r] = e ? 0u : (h[r].x == CODEC_CONSTANT ? 1u : 2u);
-          w = h[r].w;
-        }
-        uint32_t x = w;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-          if (lane >= o) x += y;
-        }
-        off[r] = (uint32_t)carry + x - w;
-        carry += __shfl_sync(0xffffffffu, x, 31);
-        if ((r + 1) * 32 >= (int)nblk) break;
+        if (r < rounds && lb < nblk) h[r] = hdr[b0 + lb];
       }
-      const uint64_t P = warp_publish_and_lookback(a.status, unit, carry);
-      if (P + carry > payload_words) err |= POLY_ST_LENGTH;
-      if (unit == sh.n_units - 1 && P + carry != payload_words) err |= POLY_ST_LENGTH;
-      const bool len_ok = P + carry <= payload_words;
+#pragma unroll
+      for (int r = 0; r < BPL_MAX; ++r) {
+        off[r] = 0;
+        if (r < rounds) {
+          const uint32_t lb = r * 32 + lane;
+          uint32_t w = 0;
+          if (lb < nblk) {
+            const uint32_t nb = min(L, nv - lb * L);
+            const uint32_t k = (h[r].x == CODEC_BASIC && h[r].z != 0) ? capacity_of((uint64_t)h[r].z + 1) : 1u;
+            const uint32_t e = check_block_hdr(h[r], nb, sh.width, k);
+            err |= e;
+            if (e) h[r].x = 0;  // skip the block
+            w = h[r].w;
+          }
+          const uint32_t x = warp_incl_scan(w);
+          off[r] = carry + x - w;
+          carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+      }
+      warp_publish_agg(a.status, unit, carry);
+      const uint64_t P = warp_lookback(a.status, unit, carry);
+      const bool len_ok = P + carry <= payload_words && carry <= sh.words_cap;
+      if (!len_ok || (unit == sh.n_units - 1 && P + carry != payload_words)) err |= POLY_ST_LENGTH;
+      if (len_ok) warp_words_in(sw, pay + P, carry);
+      __syncwarp();
 #pragma unroll
       for (int r = 0; r < BPL_MAX; ++r) {
         const uint32_t lb = r * 32 + lane;
-        if (lb < nblk && ok[r] && len_ok) {
+        if (r < rounds && lb < nblk && h[r].x != 0 && len_ok) {
           const uint32_t nb = min(L, nv - lb * L);
           V* dst = so + lb * L;
-          if (ok[r] == 1) {
+          if (h[r].x == CODEC_CONSTANT) {
             for (uint32_t i = 0; i < nb; ++i) dst[i] = (V)h[r].y;
           } else {
             const DecConst c = dec_const_of((uint64_t)h[r].z + 1);
-            const uint64_t* src = pay + P + off[r];
-            for (uint32_t j = 0; j < h[r].w; ++j) {
-              const uint32_t first = j * c.k;
-              err |= decode_any<V>(ldg_nc_u64(src + j), c, h[r].z, min(c.k, nb - first), h[r].y, dst + first);
-            }
+            const uint32_t k = dc_k(c);
+            const uint64_t* src = sw + off[r];
+            for (uint32_t j = 0, first = 0; j < h[r].w; ++j, first += k)
+              err |= decode_any<V>(src[j], c, h[r].z, min(k, nb - first), h[r].y, dst + first);
           }
         }
-        if ((r + 1) * 32 >= (int)nblk) break;
       }
     } else {
-      // warp per block: all lanes read each header (broadcast loads)
-      uint64_t total = 0;
+      // warp per block: every lane reads each header (broadcast loads)
       uint32_t* st = reinterpret_cast<uint32_t*>(slice + sh.slice - 16 * 32);
+      uint64_t total = 0;
       for (uint32_t lb = 0; lb < nblk; ++lb) {
         const uint4 h = hdr[b0 + lb];
         const uint32_t nb = min(L, nv - lb * L);
@@ -496,13 +600,13 @@ __global__ void __launch_bounds__(WARPS * 32) poly_decompress_warp(WarpArgs a) {
         }
         total += h.w;
       }
+      warp_publish_agg(a.status, unit, total);
+      const uint64_t P = warp_lookback(a.status, unit, total);
       __syncwarp();
-      const uint64_t P = warp_publish_and_lookback(a.status, unit, total);
-      if (lane == 0) {
-        if (P + total > payload_words) err |= POLY_ST_LENGTH;
-        if (unit == sh.n_units - 1 && P + total != payload_words) err |= POLY_ST_LENGTH;
-      }
-      if (P + total <= payload_words) {
+      const bool len_ok = P + total <= payload_words;
+      if (lane == 0 && (!len_ok || (unit == sh.n_units - 1 && P + total != payload_words)))
+        err |= POLY_ST_LENGTH;
+      if (len_ok) {
         for (uint32_t lb = 0; lb < nblk; ++lb) {
           const uint32_t okb = st[4 * lb + 1];
           if (!okb) continue;
@@ -514,11 +618,15 @@ __global__ void __launch_bounds__(WARPS * 32) poly_decompress_warp(WarpArgs a) {
             continue;
           }
           const DecConst c = dec_const_of((uint64_t)h.z + 1);
+          const uint32_t k = dc_k(c);
           const uint64_t* src = pay + P + st[4 * lb];
-          for (uint32_t j = lane; j < h.w; j += 32) {
-            const uint32_t first = j * c.k;
-            err |= decode_any<V>(ldg_nc_u64(src + j), c, h.z, min(c.k, nb - first), h.y, dst + first);
+          uint32_t j = lane;
+          for (; j + 32 < h.w; j += 64) {  // two words in flight per lane
+            const uint64_t s0 = ldg_nc_u64(src + j), s1 = ldg_nc_u64(src + j + 32);
+            err |= decode_any<V>(s0, c, h.z, min(k, nb - j * k), h.y, dst + j * k);
+            err |= decode_any<V>(s1, c, h.z, min(k, nb - (j + 32) * k), h.y, dst + (j + 32) * k);
           }
+          if (j < h.w) err |= decode_any<V>(ldg_nc_u64(src + j), c, h.z, min(k, nb - j * k), h.y, dst + j * k);
         }
       }
     }
