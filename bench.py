@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU work for the oracle sample")
     p.add_argument("--verify", action="store_true", help="check the stream against the oracle first")
+    p.add_argument("--no-roundtrip-check", action="store_true",
+                   help="timing experiments (POLY_DEBUG) only: skip the round-trip check")
     return p.parse_args()
 
 
@@ -227,7 +229,7 @@ def run_ours(args, rank, world, local):
     pc.poly_decompress(out, int_nbytes, dt, n, L, out=y, status=st, workspace=ws)
     torch.cuda.synchronize()
     ok = int(st.item()) == 0 and torch.equal(x, y)
-    if not ok:
+    if not ok and not args.no_roundtrip_check:
         raise SystemExit("round trip failed on rank %d (status %d)" % (rank, int(st.item())))
     if args.verify and rank == 0:
         from oracle import coracle

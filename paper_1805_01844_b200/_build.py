@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpolycomp.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 SOURCES = ["poly.cu"]
-DEPS = ["poly.cu", "poly_common.cuh", "poly_compress.cuh", "poly_decompress.cuh", "poly_warp.cuh"]
+DEPS = ["poly.cu", "poly_common.cuh", "poly_compress.cuh", "poly_decompress.cuh", "poly_warp.cuh", "poly_word.cuh", "poly_pipe.cuh", "poly_kword.cuh"]
 
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -2,6 +2,7 @@
 // checks, regime selection, table upload, kernel launches.  One translation
 // unit (the device tables are module globals).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -9,12 +10,13 @@
 #include "poly_compress.cuh"
 #include "poly_decompress.cuh"
 #include "poly_warp.cuh"
+#include "poly_pipe.cuh"
 
 using namespace polyk;
 
 namespace {
 
-enum Regime { WARP = 0, LARGE = 1 };
+enum Regime { WARP = 0, LARGE = 1, PIPE = 2 };
 
 constexpr int MAX_DEVICES = 64;
 std::mutex g_mu;
@@ -114,6 +116,15 @@ poly_status_t ensure_init(int dev) {
   set_smem_attr(poly_decompress_warp<uint16_t, 1>, wmax);
   set_smem_attr(poly_decompress_warp<uint32_t, 0>, wmax);
   set_smem_attr(poly_decompress_warp<uint32_t, 1>, wmax);
+  const int pmax = 227 * 1024;
+  set_smem_attr(poly_compress_pipe<uint16_t, 0>, pmax);
+  set_smem_attr(poly_compress_pipe<uint16_t, 1>, pmax);
+  set_smem_attr(poly_compress_pipe<uint32_t, 0>, pmax);
+  set_smem_attr(poly_compress_pipe<uint32_t, 1>, pmax);
+  set_smem_attr(poly_decompress_pipe<uint16_t, 0>, pmax);
+  set_smem_attr(poly_decompress_pipe<uint16_t, 1>, pmax);
+  set_smem_attr(poly_decompress_pipe<uint32_t, 0>, pmax);
+  set_smem_attr(poly_decompress_pipe<uint32_t, 1>, pmax);
   set_smem_attr(poly_compress_pack<uint16_t>, large_smem_pack<uint16_t>());
   set_smem_attr(poly_compress_pack<uint32_t>, large_smem_pack<uint32_t>());
   set_smem_attr(poly_decompress_unpack<uint16_t>, large_smem_unpack<uint16_t>());
@@ -129,6 +140,77 @@ poly_status_t ensure_init(int dev) {
 // arguments always give the same shape (the stream does not depend on it).
 constexpr uint32_t WT_TARGET = 4096;  // input bytes per warp unit (target)
 
+constexpr uint32_t PIPE_TILE_TARGET = 32768;  // value bytes per tile (target)
+constexpr uint32_t PIPE_SMEM_MAX = 227 * 1024;  // one CTA per SM
+
+uint32_t r16(uint64_t x) { return (uint32_t)((x + 15) / 16 * 16); }
+
+// Tile shape and shared-memory layout of the pipeline kernels (poly_pipe.cuh).
+bool plan_pipe(const Shape& sh, PipeShape& ps, bool decomp) {
+  memset(&ps, 0, sizeof ps);
+  ps.n = sh.n;
+  ps.Le = sh.Le;
+  ps.n_blocks = sh.n_blocks;
+  ps.block_len = sh.block_len;
+  ps.width = sh.width;
+  ps.vb = sh.width / 8;
+  const uint64_t bb = sh.Le * ps.vb;
+  const uint64_t kmin = sh.width == 16 ? 4 : 2;
+  if (bb <= LANE_BLOCK_MAX) {
+    ps.map = 0;
+    uint64_t bpt = PIPE_TILE_TARGET / (PC * bb);
+    bpt = std::max<uint64_t>(1, std::min<uint64_t>(BPT_MAX, bpt));
+    ps.bpt = (uint32_t)bpt;
+    ps.TB = (uint32_t)(PC * bpt);
+  } else {
+    ps.map = 1;
+    uint64_t tb = PIPE_TILE_TARGET / bb;
+    tb = std::max<uint64_t>(1, std::min<uint64_t>(256, tb));
+    ps.TB = (uint32_t)tb;
+    uint32_t G = 1;
+    while (ps.TB * G * 2 <= (uint32_t)NCW) G *= 2;
+    ps.G = G;
+    ps.Lp = (uint32_t)(((sh.Le + G - 1) / G + 7) / 8 * 8);
+  }
+  ps.tile_bytes = (uint32_t)(ps.TB * bb);
+  ps.words_cap = (uint32_t)(ps.TB * ((sh.Le + kmin - 1) / kmin));
+  ps.n_tiles = (sh.n_blocks + ps.TB - 1) / ps.TB;
+  if (ps.n_tiles >= (1ull << 32)) return false;
+  const uint32_t ctl = (uint32_t)((sizeof(PipeCtl) + 127) / 128 * 128);
+  const uint32_t cache = cache_bytes(decomp);
+  ps.o_cache = ctl;
+  const uint32_t base = ctl + cache;
+  if (!decomp) {
+    // input ring (S stages) + word ring (the rest, >= 2 worst-case tiles)
+    const uint32_t stage = r16(ps.tile_bytes) + 128;  // slack: the top-word pack may read past a block
+    const uint32_t tile_words = r16(8ull * ps.words_cap + 16);
+    int64_t room = (int64_t)PIPE_SMEM_MAX - base - 2 * (int64_t)tile_words;
+    if (room < 2 * (int64_t)stage) return false;
+    ps.S = (uint32_t)std::min<int64_t>(4, room / stage);
+    ps.in_stride = stage;
+    ps.o_in = base;
+    ps.o_ring = base + ps.S * stage;
+    ps.ring_bytes = (PIPE_SMEM_MAX - ps.o_ring) / 16 * 16;
+    ps.smem = ps.o_ring + ps.ring_bytes;
+  } else {
+    ps.o_off = 16 * ps.TB;
+    const uint32_t stage = ps.o_off + r16(4ull * ps.TB);
+    const uint32_t outb = r16(ps.tile_bytes);
+    const uint32_t tile_pay = r16(8ull * (ps.words_cap + 2));
+    const int64_t room = (int64_t)PIPE_SMEM_MAX - base - 2 * (int64_t)outb - 2 * (int64_t)tile_pay;
+    if (room < 2 * (int64_t)stage) return false;
+    ps.S = (uint32_t)std::min<int64_t>(MAXS, room / stage);
+    ps.in_stride = stage;
+    ps.out_stride = outb;
+    ps.o_in = base;
+    ps.o_out = base + ps.S * stage;
+    ps.o_ring = ps.o_out + 2 * outb;
+    ps.ring_bytes = (PIPE_SMEM_MAX - ps.o_ring) / 16 * 16;
+    ps.smem = ps.o_ring + ps.ring_bytes;
+  }
+  return ps.smem <= PIPE_SMEM_MAX;
+}
+
 bool plan(uint64_t n, uint32_t w, uint64_t block_size, Shape& sh, WarpShape& ws, Regime& rg) {
   if (n == 0 || (w != 16 && w != 32) || block_size >= (1ull << 32)) return false;
   memset(&sh, 0, sizeof sh);
@@ -140,27 +222,10 @@ bool plan(uint64_t n, uint32_t w, uint64_t block_size, Shape& sh, WarpShape& ws,
   sh.n_blocks = (n + sh.Le - 1) / sh.Le;
   if (sh.n_blocks >= (1ull << 32)) return false;
   const uint64_t bb = sh.Le * (w / 8);  // bytes per block
-  if (bb <= WT_MAX) {
-    rg = WARP;
-    ws.n = n; ws.Le = sh.Le; ws.n_blocks = sh.n_blocks; ws.block_len = sh.block_len; ws.width = w;
-    const uint64_t kmin = w == 16 ? 4 : 2;
-    if (bb <= LANE_BLOCK_MAX) {
-      ws.mode = 0;
-      uint64_t bpl = WT_TARGET / (32 * bb);
-      bpl = std::max<uint64_t>(1, std::min<uint64_t>(BPL_MAX, bpl));
-      ws.WB = (uint32_t)(32 * bpl);
-      ws.words_off = (uint32_t)((ws.WB * bb + 15) / 16 * 16);
-      ws.words_cap = (uint32_t)(ws.WB * ((sh.Le + kmin - 1) / kmin));
-      ws.slice = ws.words_off + 8 * ws.words_cap;
-    } else {
-      ws.mode = 1;
-      uint64_t wb = WT_TARGET / bb;
-      wb = std::max<uint64_t>(1, std::min<uint64_t>(32, wb));
-      ws.WB = (uint32_t)wb;
-      ws.slice = (uint32_t)((ws.WB * bb + 15) / 16 * 16 + 512);
-    }
-    ws.n_units = (sh.n_blocks + ws.WB - 1) / ws.WB;
-    if (ws.n_units >= (1ull << 32)) return false;
+  PipeShape pc, pd;
+  if (bb <= PIPE_MAX_BLOCK && plan_pipe(sh, pc, false) && plan_pipe(sh, pd, true)) {
+    rg = PIPE;
+    sh.n_chunks = pc.n_tiles;  // tiles (look-back units)
   } else {
     rg = LARGE;
     sh.cpb = (sh.Le + CH_VALUES - 1) / CH_VALUES;
@@ -180,6 +245,8 @@ WsLayout ws_layout(const Shape& sh, const WarpShape& ws, Regime rg) {
   L.status_off = 64;
   if (rg == WARP) {
     L.total = 64 + 8 * ws.n_units;
+  } else if (rg == PIPE) {
+    L.total = 64 + 8 * sh.n_chunks;
   } else {
     L.bmin_off = (64 + 8 * sh.n_stiles + 15) / 16 * 16;
     L.bmax_off = (L.bmin_off + 4 * sh.n_blocks + 15) / 16 * 16;
@@ -210,6 +277,22 @@ int warp_grid(K kernel, uint32_t smem, uint64_t units, int dev) {
   const uint64_t cap = (uint64_t)(g_sms[dev] > 0 ? g_sms[dev] : 148) * per_sm;
   const uint64_t need = (units + WARPS - 1) / WARPS;
   return (int)std::max<uint64_t>(1, std::min<uint64_t>(cap, need));
+}
+
+// POLY_DEBUG (timing experiments only; the output is then wrong): bit 0 skips
+// the per-block compute, bit 1 the look-back.
+uint32_t debug_flags() {
+  const char* e = getenv("POLY_DEBUG");
+  return e ? (uint32_t)strtoul(e, nullptr, 0) : 0u;
+}
+
+template <typename K>
+int pipe_grid(K kernel, uint32_t smem, uint64_t tiles, int dev) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, PT, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  const uint64_t cap = (uint64_t)(g_sms[dev] > 0 ? g_sms[dev] : 148) * per_sm;
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>(cap, tiles));
 }
 
 }  // namespace
@@ -257,7 +340,7 @@ int poly_launches_per_call(uint64_t n, poly_dtype_t dt, uint64_t block_size, int
   WarpShape ws;
   Regime rg;
   if (!plan(n, (uint32_t)dt, block_size, sh, ws, rg)) return 0;
-  if (rg == WARP) return 1;
+  if (rg == WARP || rg == PIPE) return 1;
   return decompress ? 2 : 3;
 }
 
@@ -293,7 +376,22 @@ poly_status_t poly_compress(const void* d_in, uint64_t n, poly_dtype_t dt, uint6
   a.ticket = reinterpret_cast<uint32_t*>(ws);
   a.status = reinterpret_cast<uint64_t*>(ws + W.status_off);
   a.sh = sh;
-  if (rg == WARP) {
+  if (rg == PIPE) {
+    cudaMemsetAsync(ws, 0, W.total, s);
+    PipeArgs pa;
+    memset(&pa, 0, sizeof pa);
+    plan_pipe(sh, pa.sh, false);
+    pa.in = reinterpret_cast<const uint8_t*>(d_in);
+    pa.out = a.out;
+    pa.compressed_bytes = d_compressed_bytes;
+    pa.status = a.status;
+    pa.ticket = a.ticket;
+    pa.bulk = ((reinterpret_cast<uintptr_t>(d_in) & 15) == 0 && pa.sh.tile_bytes % 16 == 0) ? 1u : 0u;
+    pa.debug = debug_flags();
+    auto k = dt == POLY_U16 ? (pa.sh.map == 0 ? poly_compress_pipe<uint16_t, 0> : poly_compress_pipe<uint16_t, 1>)
+                            : (pa.sh.map == 0 ? poly_compress_pipe<uint32_t, 0> : poly_compress_pipe<uint32_t, 1>);
+    k<<<pipe_grid(k, pa.sh.smem, pa.sh.n_tiles, dev), PT, pa.sh.smem, s>>>(pa);
+  } else if (rg == WARP) {
     cudaMemsetAsync(ws, 0, W.total, s);
     WarpArgs wa;
     memset(&wa, 0, sizeof wa);
@@ -381,7 +479,24 @@ poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_
   a.status = reinterpret_cast<uint64_t*>(ws + W.status_off);
   a.sh = sh;
   cudaMemsetAsync(d_status, 0, 4, s);
-  if (rg == WARP) {
+  if (rg == PIPE) {
+    cudaMemsetAsync(ws, 0, W.total, s);
+    PipeArgs pa;
+    memset(&pa, 0, sizeof pa);
+    plan_pipe(sh, pa.sh, true);
+    pa.in = a.in;
+    pa.out = reinterpret_cast<uint8_t*>(d_out);
+    pa.in_bytes = compressed_bytes;
+    pa.status_out = d_status;
+    pa.status = a.status;
+    pa.ticket = a.ticket;
+    pa.bulk = ((reinterpret_cast<uintptr_t>(d_out) & 15) == 0 && pa.sh.tile_bytes % 16 == 0) ? 1u : 0u;
+    pa.debug = debug_flags();
+    auto k = dt == POLY_U16
+                 ? (pa.sh.map == 0 ? poly_decompress_pipe<uint16_t, 0> : poly_decompress_pipe<uint16_t, 1>)
+                 : (pa.sh.map == 0 ? poly_decompress_pipe<uint32_t, 0> : poly_decompress_pipe<uint32_t, 1>);
+    k<<<pipe_grid(k, pa.sh.smem, pa.sh.n_tiles, dev), PT, pa.sh.smem, s>>>(pa);
+  } else if (rg == WARP) {
     cudaMemsetAsync(ws, 0, W.total, s);
     WarpArgs wa;
     memset(&wa, 0, sizeof wa);

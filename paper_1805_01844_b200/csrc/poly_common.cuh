@@ -213,6 +213,56 @@ __device__ __forceinline__ uint64_t lookback(const uint64_t* status, uint64_t ti
   }
 }
 
+// Wide decoupled look-back: 32 lanes x LB_PER tiles per window read (the
+// window must outgrow (tile rate x L2 round trip), or the walk to the nearest
+// inclusive prefix lengthens with the number of tiles in flight).  Same
+// contract as lookback(): all 32 lanes call it for tile >= 1 after the tile
+// published its aggregate; returns the exclusive prefix in every lane.
+constexpr int LB_PER = 8;
+__device__ __forceinline__ uint64_t lookback_wide(const uint64_t* status, uint64_t tile) {
+  const int lane = threadIdx.x & 31;
+  uint64_t excl = 0;
+  int64_t base = (int64_t)tile - 1;  // lane l covers base - LB_PER*l - j, j = 0..LB_PER-1
+  uint32_t ns = 0;
+  while (true) {
+    uint64_t e[LB_PER];
+    const int64_t top = base - (int64_t)LB_PER * lane;
+#pragma unroll
+    for (int j = 0; j < LB_PER; ++j) {
+      const int64_t idx = top - j;
+      e[j] = idx >= 0 ? ld_relaxed_u64(status + idx) : FLAG_PRE;  // before tile 0: prefix 0
+    }
+    uint32_t fpre = LB_PER, finv = LB_PER;
+#pragma unroll
+    for (int j = LB_PER - 1; j >= 0; --j) {
+      if (e[j] & FLAG_PRE) fpre = j;
+      if ((e[j] >> 62) == 0) finv = j;
+    }
+    const uint32_t bpre = __ballot_sync(0xffffffffu, fpre < LB_PER);
+    const uint32_t binv = __ballot_sync(0xffffffffu, finv < LB_PER);
+    const int lp = bpre ? __ffs(bpre) - 1 : 32, li = binv ? __ffs(binv) - 1 : 32;
+    const uint32_t ppre = bpre ? LB_PER * lp + __shfl_sync(0xffffffffu, fpre, lp) : 0xffffffffu;
+    const uint32_t pinv = binv ? LB_PER * li + __shfl_sync(0xffffffffu, finv, li) : 0xffffffffu;
+    if (bpre && ppre < pinv) {
+      uint64_t sum = 0;
+#pragma unroll
+      for (int j = 0; j < LB_PER; ++j)
+        if ((uint32_t)(LB_PER * lane + j) <= ppre) sum += e[j] & VAL_MASK;
+      return excl + warp_sum_u64(sum);
+    }
+    if (binv) {
+      if (ns) __nanosleep(ns);
+      ns = ns ? min(ns * 2, 128u) : 32u;
+      continue;
+    }
+    uint64_t sum = 0;
+#pragma unroll
+    for (int j = 0; j < LB_PER; ++j) sum += e[j] & VAL_MASK;
+    excl += warp_sum_u64(sum);
+    base -= 32 * LB_PER;
+  }
+}
+
 __device__ __forceinline__ uint32_t shfl_min(uint32_t v, int w) {
   for (int o = w >> 1; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;

@@ -1,0 +1,923 @@
+// poly_pipe.cuh -- persistent, warp-specialized pipeline kernels for blocks of
+// up to PIPE_MAX_BLOCK bytes (cfg2, cfg4, cfg5).
+//
+// One CTA per SM (persistent grid).  A tile is TB consecutive blocks; tiles
+// are handed out in increasing order by an atomic ticket, so the single-pass
+// decoupled look-back over tiles (a4 / a7) always terminates.
+//
+// compress (warps 0..NCW-1 consumers, NCW producer, NCW+1 writer):
+//   producer : ticket -> 1-D TMA bulk copy of the tile's values into a ring of
+//              S shared-memory stages (mbarrier complete_tx)
+//   consumers: per-block min/max, B, k, n_words (a2, a3); block headers go
+//              straight to global memory (fixed offsets); CTA scan of n_words;
+//              publish the tile aggregate; Horner-pack the words (a5) into one
+//              of two staging buffers
+//   writer   : look back for the tile's payload offset, publish the inclusive
+//              prefix, copy the staged words to the stream with coalesced
+//              16-byte stores (a4, a6); the last tile writes the global header
+// decompress (warps 0..NCW-1 consumers, NCW header loader, NCW+1 look-back):
+//   header loader : ticket -> TMA bulk copy of the tile's block headers into
+//              one of SH header stages (deep prefetch: headers are small)
+//   look-back warp: n_words sum and in-tile offsets, publish the aggregate,
+//              look back, then TMA bulk copy of the tile's payload words into
+//              a shared-memory ring buffer (allocated by size, not worst case)
+//   consumers: validate headers (a9), extract digits without integer divides
+//              (a8) into a staging buffer, TMA bulk store of the decoded tile.
+#pragma once
+#include "poly_common.cuh"
+#include "poly_word.cuh"
+#include "poly_kword.cuh"
+
+namespace polyk {
+
+constexpr int NCW = 16;            // consumer warps
+constexpr int PC = NCW * 32;       // consumer threads
+constexpr int PT = PC + 96;        // + producer, writer and header-sum warps
+constexpr int W_PROD = NCW;        // warp index of the producer / header issuer
+constexpr int W_WRIT = NCW + 1;    // warp index of the writer / look-back warp
+constexpr int W_HSUM = NCW + 2;    // decompress: header-sum warp (compress: idle)
+constexpr int MAXS = 8;            // max ring stages
+constexpr int BPT_MAX = 2;         // map 0: blocks per consumer thread
+constexpr uint32_t PIPE_MAX_BLOCK = 32768;  // bytes per block handled here
+constexpr uint32_t CACHE_B = 512;  // shared-memory cache of per-base constants
+constexpr uint64_t TILE_NONE = ~0ull;
+constexpr int BAR_CONS = 1;        // named barrier id of the consumer warps
+
+struct PipeShape {
+  uint64_t n, Le, n_blocks, n_tiles;
+  uint32_t block_len, width, vb;
+  uint32_t TB;          // blocks per tile
+  uint32_t map;         // 0: one consumer thread per block; 1: G warps per block
+  uint32_t bpt;         // map 0: blocks per consumer thread
+  uint32_t G;           // map 1: warps per block (power of two)
+  uint32_t Lp;          // map 1: values per part (G parts per block)
+  uint32_t tile_bytes;  // value bytes of a full tile
+  uint32_t words_cap;   // payload words a tile can hold (any valid stream)
+  uint32_t S;           // ring stages (compress input / decompress header stages)
+  uint32_t in_stride;   // bytes per stage
+  uint32_t out_stride;  // bytes per staging buffer (two of them)
+  uint32_t o_off;       // decompress: offset of OFF[] inside a header stage (HDR at 0)
+  uint32_t o_cache;     // offset of the base-constant cache
+  uint32_t o_in, o_out; // offsets of the stages and the staging buffers
+  uint32_t o_ring, ring_bytes;  // decompress: payload ring
+  uint32_t smem;        // dynamic shared memory bytes
+};
+
+struct PipeArgs {
+  const uint8_t* in;        // compress: values; decompress: stream
+  uint8_t* out;             // compress: stream; decompress: values
+  uint64_t* compressed_bytes;
+  uint64_t in_bytes;        // decompress: stream length
+  uint32_t* status_out;     // decompress: caller's status word
+  uint64_t* status;         // look-back words, one per tile
+  uint32_t* ticket;
+  uint32_t bulk;            // value array 16-byte aligned and tile_bytes % 16 == 0
+  uint32_t debug;           // timing experiments only (POLY_DEBUG): 1 skip compute, 2 skip look-back
+  PipeShape sh;
+};
+
+constexpr int MAXR = 8;            // compress: records in flight (consumers -> writer)
+
+struct __align__(16) PipeCtl {
+  uint64_t full_in[MAXS], empty_in[MAXS], hbar[MAXS], aggr[MAXS];
+  uint64_t rec_full[MAXR], rec_empty[MAXR];
+  uint64_t tkt[MAXS];       // ticket of the tile held by each stage
+  uint64_t W[MAXS];         // decompress: payload words of the stage's tile
+  uint64_t P[MAXS];         // decompress: payload word prefix of the stage's tile
+  uint64_t ring_end[MAXS];  // decompress: ring position after the stage's payload
+  uint32_t ring_off[MAXS];  // decompress: byte offset of the stage's payload in the ring
+  uint32_t err[MAXS];       // decompress: tile-level status bits
+  uint64_t rec_t[MAXR], rec_W[MAXR], rec_end[MAXR];  // compress: staged tiles
+  uint32_t rec_off[MAXR];
+  uint32_t cur_off;         // compress: ring offset of the tile being packed
+  uint64_t payload_words;
+  volatile uint64_t ring_tail;  // ring bytes released (compress: by the writer; decompress: by the consumers)
+  uint32_t hdr_err, pad;
+  uint32_t scan[2][NCW];
+  uint32_t smin[256], smax[256];                        // map 1: partial min / max per segment
+  uint32_t bvmin[256], bbm1[256], bnw[256], boff[256];  // map 1: per-block results
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(tx)
+               : "memory");
+}
+// Wait for the phase with the given parity to complete.  The suspend-time hint
+// parks the thread in the barrier unit instead of spinning on issue slots.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// 1-D bulk copy global -> shared (both 16-byte aligned, bytes % 16 == 0).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// 1-D bulk copy shared -> global (bulk group).
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void cons_bar() { asm volatile("bar.sync %0, %1;" ::"n"(BAR_CONS), "n"(PC) : "memory"); }
+
+// Exclusive scan of x over the PC consumer threads; *total = sum.  `buf`
+// alternates between calls (a call's barrier protects the buffer of the
+// call before it).
+__device__ __forceinline__ uint32_t cons_scan(uint32_t x, uint32_t* total, uint32_t* buf) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t inc = warp_incl_scan(x);
+  if (lane == 31) buf[warp] = inc;
+  cons_bar();
+  const uint32_t ws = lane < NCW ? buf[lane] : 0u;
+  const uint32_t wi = warp_incl_scan(ws);
+  *total = __shfl_sync(0xffffffffu, wi, NCW - 1);
+  const uint32_t wex = __shfl_sync(0xffffffffu, wi - ws, warp);
+  return wex + inc - x;
+}
+
+// ------------------------------------------------------------------ base constants
+// Shared-memory cache of the per-base table for B <= CACHE_B (SoA so that
+// lanes with nearby bases hit different banks).  cmeta = DecConst.meta
+// (k | log2b << 8 | t32 << 16 | h << 24).
+struct BaseCache {
+  uint32_t* meta;
+  uint64_t* Bk;  // decompress: B^k
+  uint64_t* Rl;  // decompress: ceil(2^160 / B^k), low / high 64 bits
+  uint64_t* Rh;
+  uint64_t* D;   // compress: B^h
+  uint32_t* G;   // compress: 1 + B + ... + B^(h-1) mod 2^32
+};
+
+__device__ __forceinline__ BaseCache cache_at(uint8_t* base, bool dec) {
+  BaseCache c;
+  uint64_t* p = reinterpret_cast<uint64_t*>(base);
+  if (dec) {
+    c.Bk = p;
+    c.Rl = p + (CACHE_B + 1);
+    c.Rh = p + 2 * (CACHE_B + 1);
+    c.meta = reinterpret_cast<uint32_t*>(p + 3 * (CACHE_B + 1));
+    c.D = nullptr;
+    c.G = nullptr;
+  } else {
+    c.D = p;
+    c.meta = reinterpret_cast<uint32_t*>(p + (CACHE_B + 1));
+    c.G = c.meta + (CACHE_B + 1);
+    c.Bk = c.Rl = c.Rh = nullptr;
+  }
+  return c;
+}
+__host__ __device__ constexpr uint32_t cache_bytes(bool dec) {
+  return dec ? (uint32_t)(3 * 8 * (CACHE_B + 1) + 4 * (CACHE_B + 1) + 15) / 16 * 16
+             : (uint32_t)(8 * (CACHE_B + 1) + 8 * (CACHE_B + 1) + 15) / 16 * 16;
+}
+__device__ __forceinline__ void cache_fill(const BaseCache& c, bool dec) {
+  for (uint32_t B = threadIdx.x; B <= CACHE_B; B += blockDim.x) {
+    const DecConst d = g_dtab[B];
+    c.meta[B] = d.meta;
+    if (dec) {
+      c.Bk[B] = d.Bk;
+      c.Rl[B] = d.Rl;
+      c.Rh[B] = d.Rh;
+    } else {
+      const uint32_t h = d.meta >> 24;
+      uint64_t D = 1;
+      uint32_t G = 0;
+      for (uint32_t i = 0; i < h; ++i) {
+        G = G * B + 1u;
+        D *= B;
+      }
+      c.D[B] = D;
+      c.G[B] = G;
+    }
+  }
+}
+// Chunk constants of the pack: D = B^h and G = 1 + B + ... + B^(h-1) mod 2^32.
+__device__ __forceinline__ void chunk_consts(const BaseCache& c, uint32_t B, uint32_t h, uint64_t& D, uint32_t& G) {
+  if (B <= CACHE_B) {
+    D = c.D[B];
+    G = c.G[B];
+    return;
+  }
+  D = 1;
+  G = 0;
+  for (uint32_t i = 0; i < h; ++i) {
+    G = G * B + 1u;
+    D *= B;
+  }
+}
+// k (values per u64 word) for 2 <= B <= 2^32.
+__device__ __forceinline__ uint32_t k_of(const BaseCache& c, uint64_t B) {
+  if (B <= CACHE_B) return c.meta[B] & 0xffu;
+  return capacity_of(B);
+}
+// k and h (values per 32-bit chunk) for 2 <= B <= 2^16.
+__device__ __forceinline__ uint32_t kh_of16(const BaseCache& c, uint32_t B) {
+  const uint32_t m = B <= CACHE_B ? c.meta[B] : g_dtab[B].meta;
+  return (m & 0xffu) | ((m >> 16) & 0xff00u);  // k | h << 8
+}
+__device__ __forceinline__ DecConst dconst_of(const BaseCache& c, uint64_t B) {
+  if (B <= CACHE_B) {
+    DecConst d;
+    d.Bk = c.Bk[B];
+    d.Rl = c.Rl[B];
+    d.Rh = c.Rh[B];
+    d.meta = c.meta[B];
+    d.pad = 0;
+    return d;
+  }
+  return dec_const_of(B);
+}
+
+// min / max of n values at s by one warp (16-byte vector loads when aligned).
+template <typename V>
+__device__ __forceinline__ void warp_minmax(const V* s, uint32_t n, uint32_t& mn, uint32_t& mx) {
+  const int lane = threadIdx.x & 31;
+  mn = 0xffffffffu;
+  mx = 0u;
+  uint32_t i0 = 0;
+  if ((reinterpret_cast<uintptr_t>(s) & 15) == 0) {
+    const uint4* q = reinterpret_cast<const uint4*>(s);
+    constexpr uint32_t PER = 16 / sizeof(V);
+    const uint32_t nq = n / PER;
+    if (sizeof(V) == 2) {
+      uint32_t a0 = 0xffffffffu, a1 = 0u;
+#pragma unroll 4
+      for (uint32_t i = lane; i < nq; i += 32) {
+        const uint4 t = q[i];
+        a0 = __vimin3_u16x2(a0, t.x, t.y);
+        a0 = __vimin3_u16x2(a0, t.z, t.w);
+        a1 = __vimax3_u16x2(a1, t.x, t.y);
+        a1 = __vimax3_u16x2(a1, t.z, t.w);
+      }
+      mn = min(a0 & 0xffffu, a0 >> 16);
+      mx = max(a1 & 0xffffu, a1 >> 16);
+    } else {
+#pragma unroll 4
+      for (uint32_t i = lane; i < nq; i += 32) {
+        const uint4 t = q[i];
+        mn = min(min(mn, t.x), min(t.y, min(t.z, t.w)));
+        mx = max(max(mx, t.x), max(t.y, max(t.z, t.w)));
+      }
+    }
+    i0 = nq * PER;
+  }
+  for (uint32_t i = i0 + lane; i < n; i += 32) {
+    mn = min(mn, (uint32_t)s[i]);
+    mx = max(mx, (uint32_t)s[i]);
+  }
+  mn = shfl_min(mn, 32);
+  mx = shfl_max(mx, 32);
+}
+
+// Copy nbytes global -> shared by one warp (16-byte vectors when both allow).
+__device__ __forceinline__ void warp_copy(uint8_t* dst, const uint8_t* src, uint32_t nbytes, int lane) {
+  uint32_t done = 0;
+  if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+    const uint32_t n16 = nbytes >> 4;
+    for (uint32_t i = lane; i < n16; i += 32)
+      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    done = n16 << 4;
+  }
+  for (uint32_t i = done + lane; i < nbytes; i += 32) dst[i] = src[i];
+}
+
+// ======================================================================
+// compress
+// ======================================================================
+template <typename V, int MAP>
+__global__ void __launch_bounds__(PT, 1) poly_compress_pipe(PipeArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  PipeCtl& C = *reinterpret_cast<PipeCtl*>(smem);
+  const PipeShape& sh = a.sh;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t S = sh.S;
+  const BaseCache bc = cache_at(smem + sh.o_cache, false);
+  uint8_t* ring = smem + sh.o_ring;
+  if (tid == 0) {
+    for (uint32_t s = 0; s < S; ++s) {
+      mbar_init(&C.full_in[s], 1);
+      mbar_init(&C.empty_in[s], 1);
+    }
+    for (int r = 0; r < MAXR; ++r) {
+      mbar_init(&C.rec_full[r], 1);
+      mbar_init(&C.rec_empty[r], 1);
+    }
+    C.ring_tail = 0;
+    mbar_fence_init();
+  }
+  cache_fill(bc, false);
+  __syncthreads();
+  if (warp == W_HSUM) return;
+
+  if (warp == W_PROD) {
+    // ---------------------------------------------------------- producer
+    const uint64_t total_bytes = sh.n * sh.vb;
+    for (uint32_t s = 0, ph = 0;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0)) {
+      mbar_wait(&C.empty_in[s], ph ^ 1u);
+      uint32_t t32 = 0;
+      if (lane == 0) t32 = atomicAdd(a.ticket, 1u);
+      const uint64_t t = __shfl_sync(0xffffffffu, t32, 0);
+      uint8_t* dst = smem + sh.o_in + (size_t)s * sh.in_stride;
+      if (t >= sh.n_tiles) {
+        if (lane == 0) {
+          C.tkt[s] = TILE_NONE;
+          mbar_arrive(&C.full_in[s]);
+        }
+        break;
+      }
+      const uint64_t off = t * sh.tile_bytes;
+      const uint32_t bytes = (uint32_t)min((uint64_t)sh.tile_bytes, total_bytes - off);
+      const uint8_t* src = a.in + off;
+      if (a.bulk) {
+        if (lane == 0) {
+          const uint32_t b16 = bytes & ~15u;
+          C.tkt[s] = t;
+          for (uint32_t j = b16; j < bytes; ++j) dst[j] = src[j];  // last tile only
+          mbar_arrive_tx(&C.full_in[s], b16);
+          if (b16) bulk_g2s(dst, src, b16, &C.full_in[s]);
+        }
+      } else {
+        warp_copy(dst, src, bytes, lane);
+        __syncwarp();
+        if (lane == 0) {
+          C.tkt[s] = t;
+          mbar_arrive(&C.full_in[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  uint64_t* pay_g = reinterpret_cast<uint64_t*>(a.out + 32 + 16 * sh.n_blocks);
+  if (warp == W_WRIT) {
+    // ---------------------------------------------------------- writer
+    for (uint32_t i = 0;; ++i) {
+      const uint32_t r = i % MAXR, ph = (i / MAXR) & 1u;
+      mbar_wait(&C.rec_full[r], ph);
+      const uint64_t t = C.rec_t[r];
+      if (t == TILE_NONE) break;
+      const uint64_t W = C.rec_W[r];
+      uint64_t P = 0;
+      if (t != 0 && !(a.debug & 2)) {
+        P = lookback_wide(a.status, t);
+        if (lane == 0) st_relaxed_u64(a.status + t, FLAG_PRE | ((P + W) & VAL_MASK));
+      }
+      const uint64_t* src = reinterpret_cast<const uint64_t*>(ring + C.rec_off[r]);
+      uint64_t* dst = pay_g + P;
+      const uint32_t w = (uint32_t)W;
+      uint32_t j = lane;
+      for (; j + 224 < w; j += 256) {
+        uint64_t v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = src[j + 32 * q];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dst[j + 32 * q] = v[q];
+      }
+      for (; j < w; j += 32) dst[j] = src[j];
+      if (t == sh.n_tiles - 1 && lane == 0) {
+        write_global_header_f(a.out, sh.width, sh.n, sh.block_len, sh.n_blocks, P + W);
+        *a.compressed_bytes = 32 + 16 * sh.n_blocks + 8 * (P + W);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        C.ring_tail = C.rec_end[r];
+        mbar_arrive(&C.rec_empty[r]);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers
+  const int ctid = tid;  // 0 .. PC-1
+  const uint32_t L = (uint32_t)sh.Le;
+  uint4* hdr_g = reinterpret_cast<uint4*>(a.out + 32);
+  uint64_t head = 0;  // ring bytes handed out (thread 0's copy is authoritative)
+  for (uint32_t s = 0, ph = 0, r = 0, rph = 0;;
+       s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0), r = (r + 1) % MAXR, rph ^= (r == 0)) {
+    mbar_wait(&C.full_in[s], ph);
+    const uint64_t t = C.tkt[s];
+    if (t == TILE_NONE) {
+      if (ctid == 0) {
+        mbar_wait(&C.rec_empty[r], rph ^ 1u);
+        C.rec_t[r] = TILE_NONE;
+        mbar_arrive(&C.rec_full[r]);
+      }
+      break;
+    }
+    const V* sv = reinterpret_cast<const V*>(smem + sh.o_in + (size_t)s * sh.in_stride);
+    const uint64_t b0 = t * sh.TB;
+    const uint32_t nblk = (uint32_t)min((uint64_t)sh.TB, sh.n_blocks - b0);
+    const uint64_t v0 = b0 * sh.Le;
+    const uint32_t nv = (uint32_t)(min(sh.n, v0 + (uint64_t)sh.TB * sh.Le) - v0);
+    uint32_t W = 0;
+    uint32_t vmin[BPT_MAX], bm1[BPT_MAX], nw[BPT_MAX], kk[BPT_MAX], off[BPT_MAX];
+
+    // ---- a2, a3: block statistics, headers, in-tile word offsets
+    if (a.debug & 1) {
+#pragma unroll
+      for (int q = 0; q < BPT_MAX; ++q) {
+        vmin[q] = bm1[q] = nw[q] = off[q] = 0;
+        kk[q] = 1;
+      }
+      if (MAP == 1 && ctid < (int)nblk) C.bbm1[ctid] = 0;
+    } else if (MAP == 0) {
+#pragma unroll
+      for (int q = 0; q < BPT_MAX; ++q) {
+        vmin[q] = 0;
+        bm1[q] = 0;
+        nw[q] = 0;
+        kk[q] = 1;
+        off[q] = 0;
+        if (q < (int)sh.bpt) {
+          const uint32_t b = q * PC + ctid;
+          if (b < nblk) {
+            const uint32_t nb = min(L, nv - b * L);
+            uint32_t mn, mx;
+            block_minmax<V>(sv + (size_t)b * L, nb, mn, mx);
+            vmin[q] = mn;
+            bm1[q] = mx - mn;
+            if (mx != mn) {
+              kk[q] = sizeof(V) == 2 ? kh_of16(bc, mx - mn + 1) : k_of(bc, (uint64_t)(mx - mn) + 1);
+              nw[q] = ceil_div_small(nb, kk[q] & 0xffu);
+            }
+            hdr_g[b0 + b] = make_uint4(mx == mn ? CODEC_CONSTANT : CODEC_BASIC, mn, mx - mn, nw[q]);
+          }
+          uint32_t tot;
+          off[q] = W + cons_scan(nw[q], &tot, C.scan[q & 1]);
+          W += tot;
+        }
+      }
+    } else {
+      const uint32_t G = sh.G, nseg = nblk * G;
+      for (uint32_t seg = warp; seg < nseg; seg += NCW) {
+        const uint32_t b = seg / G, part = seg % G;
+        const uint32_t nb = min(L, nv - b * L);
+        const uint32_t lo = min(nb, part * sh.Lp), hi = min(nb, lo + sh.Lp);
+        uint32_t mn, mx;
+        warp_minmax<V>(sv + (size_t)b * L + lo, hi - lo, mn, mx);
+        if (lane == 0) {
+          C.smin[seg] = mn;
+          C.smax[seg] = mx;
+        }
+      }
+      cons_bar();
+      uint32_t nwb = 0;
+      if (ctid < (int)nblk) {
+        uint32_t mn = 0xffffffffu, mx = 0u;
+        for (uint32_t p = 0; p < G; ++p) {
+          mn = min(mn, C.smin[ctid * G + p]);
+          mx = max(mx, C.smax[ctid * G + p]);
+        }
+        const uint32_t nb = min(L, nv - ctid * L);
+        if (mx != mn) nwb = ceil_div_small(nb, k_of(bc, (uint64_t)(mx - mn) + 1));
+        C.bvmin[ctid] = mn;
+        C.bbm1[ctid] = mx - mn;
+        C.bnw[ctid] = nwb;
+        hdr_g[b0 + ctid] = make_uint4(mx == mn ? CODEC_CONSTANT : CODEC_BASIC, mn, mx - mn, nwb);
+      }
+      const uint32_t ex = cons_scan(nwb, &W, C.scan[0]);
+      if (ctid < (int)nblk) C.boff[ctid] = ex;
+    }
+    // ---- a4: publish the tile aggregate, then take ring space for its words
+    if (ctid == 0) {
+      st_relaxed_u64(a.status + t, (t == 0 ? FLAG_PRE : FLAG_AGG) | W);
+      mbar_wait(&C.rec_empty[r], rph ^ 1u);
+      const uint32_t need = (8 * W + 15) & ~15u;
+      uint32_t pos = (uint32_t)(head % sh.ring_bytes);
+      if (pos + need > sh.ring_bytes) {
+        head += sh.ring_bytes - pos;
+        pos = 0;
+      }
+      uint32_t ns = 0;
+      while (head + need - C.ring_tail > sh.ring_bytes) {
+        __nanosleep(ns);
+        ns = ns ? min(ns * 2, 256u) : 32u;
+      }
+      __threadfence_block();
+      head += need;
+      C.cur_off = pos;
+      C.rec_t[r] = t;
+      C.rec_W[r] = W;
+      C.rec_off[r] = pos;
+      C.rec_end[r] = head;
+    }
+    cons_bar();
+    uint64_t* ow = reinterpret_cast<uint64_t*>(ring + C.cur_off);
+
+    // ---- a5: Horner pack
+    if (MAP == 0) {
+#pragma unroll
+      for (int q = 0; q < BPT_MAX; ++q) {
+        const uint32_t b = q * PC + ctid;
+        if (q < (int)sh.bpt && b < nblk && nw[q] != 0) {
+          const uint32_t nb = min(L, nv - b * L);
+          if (sizeof(V) == 2) {
+            const uint32_t B = bm1[q] + 1, k = kk[q] & 0xffu, h = kk[q] >> 8;
+            uint64_t D;
+            uint32_t G;
+            chunk_consts(bc, B, h, D, G);
+            pack_block_lane16(reinterpret_cast<const uint16_t*>(sv + (size_t)b * L), nb, vmin[q], B, k, h, D, G,
+                              nw[q], ow + off[q]);
+          } else {
+            pack_block_words<V>(sv + (size_t)b * L, nb, vmin[q], (uint64_t)bm1[q] + 1, kk[q], nw[q], ow + off[q]);
+          }
+        }
+      }
+    } else {
+      const uint32_t G = sh.G, nseg = nblk * G;
+      for (uint32_t seg = warp; seg < nseg; seg += NCW) {
+        const uint32_t b = seg / G, part = seg % G;
+        const uint32_t bm1b = C.bbm1[b];
+        if (bm1b == 0) continue;
+        const uint32_t nb = min(L, nv - b * L), nwk = C.bnw[b], vm = C.bvmin[b];
+        const uint64_t B = (uint64_t)bm1b + 1;
+        const uint32_t k = k_of(bc, B);
+        const V* src = sv + (size_t)b * L;
+        uint64_t* dst = ow + C.boff[b];
+        uint32_t done = 0;
+        if (sizeof(V) == 2 && ((L * 2) & 15) == 0) {
+          const uint8_t* blk = reinterpret_cast<const uint8_t*>(src);
+          switch (k) {
+#define POLY_PK(KK)                                                                              \
+  case KK:                                                                                       \
+    done = pack_block_k<KK>(blk, nb, (uint32_t)B, vm, part * 32 + lane, 32 * G, dst);            \
+    break;
+            POLY_FOR_EACH_K16(POLY_PK)
+#undef POLY_PK
+            default:
+              break;
+          }
+        }
+        for (uint32_t j = done + part * 32 + lane; j < nwk; j += 32 * G) {
+          const uint32_t first = j * k;
+          dst[j] = pack_word64<V>(src + first, min(k, nb - first), B, vm);
+        }
+      }
+    }
+    cons_bar();
+    if (ctid == 0) {
+      mbar_arrive(&C.rec_full[r]);
+      mbar_arrive(&C.empty_in[s]);
+    }
+  }
+}
+
+// ======================================================================
+// decompress
+// ======================================================================
+__device__ __forceinline__ uint32_t check_global_header_p(const PipeArgs& a, uint64_t* pw) {
+  const PipeShape& sh = a.sh;
+  *pw = 0;
+  if (a.in_bytes < 32) return POLY_ST_LENGTH;
+  const uint4 h0 = reinterpret_cast<const uint4*>(a.in)[0];
+  const uint4 h1 = reinterpret_cast<const uint4*>(a.in)[1];
+  const uint64_t n = (uint64_t)h0.z | ((uint64_t)h0.w << 32);
+  const uint64_t pb = (uint64_t)h1.z | ((uint64_t)h1.w << 32);
+  if (h0.x != 0x43594c50u) return POLY_ST_BAD_MAGIC;
+  if ((h0.y & 0xffu) != 2u) return POLY_ST_BAD_VERSION;
+  if (((h0.y >> 8) & 0xffu) != 0u || ((h0.y >> 16) & 0xffu) != sh.width || (h0.y >> 24) != 0u || n != sh.n ||
+      h1.x != sh.block_len || h1.y != (uint32_t)sh.n_blocks)
+    return POLY_ST_HEADER_MISMATCH;
+  if ((pb & 7) != 0 || a.in_bytes != 32 + 16 * sh.n_blocks + pb) return POLY_ST_LENGTH;
+  *pw = pb >> 3;
+  return 0;
+}
+
+template <typename V, int MAP>
+__global__ void __launch_bounds__(PT, 1) poly_decompress_pipe(PipeArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  PipeCtl& C = *reinterpret_cast<PipeCtl*>(smem);
+  const PipeShape& sh = a.sh;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t S = sh.S;
+  const BaseCache bc = cache_at(smem + sh.o_cache, true);
+  uint8_t* ring = smem + sh.o_ring;
+  if (tid == 0) {
+    for (uint32_t s = 0; s < S; ++s) {
+      mbar_init(&C.hbar[s], 1);
+      mbar_init(&C.aggr[s], 1);
+      mbar_init(&C.full_in[s], 1);
+      mbar_init(&C.empty_in[s], 1);
+    }
+    mbar_fence_init();
+    uint64_t pw;
+    C.hdr_err = check_global_header_p(a, &pw);
+    C.payload_words = pw;
+    C.ring_tail = 0;
+  }
+  cache_fill(bc, true);
+  __syncthreads();
+  if (C.hdr_err) {  // same verdict in every CTA: nothing is decoded, no look-back
+    if (blockIdx.x == 0 && tid == 0) atomicOr(a.status_out, C.hdr_err);
+    return;
+  }
+  const uint4* hdr_g = reinterpret_cast<const uint4*>(a.in + 32);
+  const uint64_t* pay_g = reinterpret_cast<const uint64_t*>(a.in + 32 + 16 * sh.n_blocks);
+
+  if (warp == W_PROD) {
+    // ---------------------------------------------------------- header issuer
+    if (lane != 0) return;
+    for (uint32_t i = 0, s = 0, ph = 0;; ++i) {
+      mbar_wait(&C.empty_in[s], ph ^ 1u);
+      const uint64_t t = atomicAdd(a.ticket, 1u);
+      if (t >= sh.n_tiles) {
+        C.tkt[s] = TILE_NONE;
+        mbar_arrive(&C.hbar[s]);
+        break;
+      }
+      C.tkt[s] = t;
+      const uint64_t b0 = t * sh.TB;
+      const uint32_t nblk = (uint32_t)min((uint64_t)sh.TB, sh.n_blocks - b0);
+      mbar_arrive_tx(&C.hbar[s], nblk * 16);
+      bulk_g2s(smem + sh.o_in + (size_t)s * sh.in_stride, hdr_g + b0, nblk * 16, &C.hbar[s]);
+      if (++s == S) {
+        s = 0;
+        ph ^= 1u;
+      }
+    }
+    return;
+  }
+
+  if (warp == W_HSUM) {
+    // ---------------------------------------------------------- header sum
+    // Publishes each tile's aggregate as soon as its headers land (a7), and
+    // the in-tile word offsets of its blocks.
+    for (uint32_t s = 0, ph = 0;;) {
+      mbar_wait(&C.hbar[s], ph);
+      const uint64_t t = C.tkt[s];
+      if (t == TILE_NONE) {
+        if (lane == 0) mbar_arrive(&C.aggr[s]);
+        break;
+      }
+      uint8_t* st = smem + sh.o_in + (size_t)s * sh.in_stride;
+      const uint4* H = reinterpret_cast<const uint4*>(st);
+      uint32_t* OFF = reinterpret_cast<uint32_t*>(st + sh.o_off);
+      const uint64_t b0 = t * sh.TB;
+      const uint32_t nblk = (uint32_t)min((uint64_t)sh.TB, sh.n_blocks - b0);
+      const uint32_t q = (nblk + 31) >> 5, lo = min(nblk, lane * q), hi = min(nblk, lo + q);
+      uint64_t sum = 0;
+      for (uint32_t b = lo; b < hi; ++b) sum += H[b].w;
+      uint64_t inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const uint64_t W = __shfl_sync(0xffffffffu, inc, 31);
+      if (W <= sh.words_cap) {
+        uint32_t ex = (uint32_t)(inc - sum);
+        for (uint32_t b = lo; b < hi; ++b) {
+          OFF[b] = ex;
+          ex += H[b].w;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        st_relaxed_u64(a.status + t, (t == 0 ? FLAG_PRE : FLAG_AGG) | (W & VAL_MASK));
+        C.W[s] = W;
+        mbar_arrive(&C.aggr[s]);
+      }
+      if (++s == S) {
+        s = 0;
+        ph ^= 1u;
+      }
+    }
+    return;
+  }
+
+  if (warp == W_WRIT) {
+    // ---------------------------------------------------------- look-back + payload loader
+    const uint64_t pw = C.payload_words;
+    uint64_t head = 0;  // ring bytes handed out (lane 0's copy is authoritative)
+    for (uint32_t s = 0, ph = 0;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0)) {
+      mbar_wait(&C.aggr[s], ph);
+      const uint64_t t = C.tkt[s];
+      if (t == TILE_NONE) {
+        if (lane == 0) mbar_arrive(&C.full_in[s]);
+        break;
+      }
+      const uint64_t W = C.W[s];
+      uint64_t P = 0;
+      if (a.debug & 2) {
+        P = min(t * (pw / sh.n_tiles), pw - min(pw, W));
+      } else if (t != 0) {
+        P = lookback_wide(a.status, t);
+        if (lane == 0) st_relaxed_u64(a.status + t, FLAG_PRE | ((P + W) & VAL_MASK));
+      }
+      uint32_t e = 0;
+      uint64_t wl = W;
+      if (W > sh.words_cap || P + W > pw) {
+        e = POLY_ST_LENGTH;
+        wl = 0;
+      }
+      if (t == sh.n_tiles - 1 && P + W != pw) e |= POLY_ST_LENGTH;
+      if (a.debug & 2) e = 0;
+      if (lane == 0) {
+        C.P[s] = P;
+        C.err[s] = e;
+        if (wl) {
+          const uint64_t a0 = P & ~1ull, hw = P + wl;
+          uint64_t a1 = min((hw + 1) & ~1ull, pw & ~1ull);
+          if (a1 < a0) a1 = a0;
+          const uint32_t need = (uint32_t)((8 * (hw - a0) + 15) & ~15ull);
+          uint32_t pos = (uint32_t)(head % sh.ring_bytes);
+          if (pos + need > sh.ring_bytes) {  // wrap: the tile's words stay contiguous
+            head += sh.ring_bytes - pos;
+            pos = 0;
+          }
+          uint32_t ns = 0;
+          while (head + need - C.ring_tail > sh.ring_bytes) {
+            __nanosleep(ns);
+            ns = ns ? min(ns * 2, 256u) : 32u;
+          }
+          __threadfence_block();
+          fence_proxy_async_smem();
+          uint64_t* dst = reinterpret_cast<uint64_t*>(ring + pos);
+          C.ring_off[s] = pos;
+          head += need;
+          C.ring_end[s] = head;
+          for (uint64_t w = a1; w < hw; ++w) dst[w - a0] = ldg_nc_u64(pay_g + w);
+          const uint32_t bytes = (uint32_t)(8 * (a1 - a0));
+          mbar_arrive_tx(&C.full_in[s], bytes);
+          if (bytes) bulk_g2s(dst, pay_g + a0, bytes, &C.full_in[s]);
+        } else {
+          C.ring_off[s] = 0;
+          C.ring_end[s] = head;
+          mbar_arrive(&C.full_in[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers
+  const int ctid = tid;
+  const uint32_t L = (uint32_t)sh.Le;
+  uint32_t err = 0;
+  for (uint32_t s = 0, ph = 0, s2 = 0;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0), s2 ^= 1u) {
+    mbar_wait(&C.full_in[s], ph);
+    const uint64_t t = C.tkt[s];
+    if (t == TILE_NONE) break;
+    const uint8_t* st = smem + sh.o_in + (size_t)s * sh.in_stride;
+    const uint4* H = reinterpret_cast<const uint4*>(st);
+    const uint32_t* OFF = reinterpret_cast<const uint32_t*>(st + sh.o_off);
+    const uint64_t* PAY = reinterpret_cast<const uint64_t*>(ring + C.ring_off[s]) + (C.P[s] & 1);
+    const uint32_t terr = C.err[s];
+    const uint64_t rend = C.ring_end[s];
+    uint8_t* ob8 = smem + sh.o_out + (size_t)s2 * sh.out_stride;
+    V* ob = reinterpret_cast<V*>(ob8);
+    const uint64_t b0 = t * sh.TB;
+    const uint32_t nblk = (uint32_t)min((uint64_t)sh.TB, sh.n_blocks - b0);
+    const uint64_t v0 = b0 * sh.Le;
+    const uint32_t nv = (uint32_t)(min(sh.n, v0 + (uint64_t)sh.TB * sh.Le) - v0);
+    const bool bst = a.bulk && !(a.debug & 4);  // TMA bulk store of the tile (else coalesced STG)
+    if (bst && ctid == 0) bulk_wait_read<1>();  // staging buffer s2 is free again
+    cons_bar();
+    if (terr == 0 && !(a.debug & 1)) {
+      if (MAP == 0) {
+        for (uint32_t q = 0; q < sh.bpt; ++q) {
+          const uint32_t b = q * PC + ctid;
+          if (b >= nblk) break;
+          const uint4 h = H[b];
+          const uint32_t nb = min(L, nv - b * L);
+          V* dst = ob + (size_t)b * L;
+          const uint32_t k = (h.x == CODEC_BASIC && h.z != 0) ? k_of(bc, (uint64_t)h.z + 1) : 1u;
+          const uint32_t e = check_block_hdr(h, nb, sh.width, k);
+          err |= e;
+          if (e) continue;
+          if (h.x == CODEC_CONSTANT) {
+            for (uint32_t j = 0; j < nb; ++j) dst[j] = (V)h.y;
+          } else {
+            const DecConst c = dconst_of(bc, (uint64_t)h.z + 1);
+            const uint64_t* src = PAY + OFF[b];
+            if (dc_log2b(c)) {
+              for (uint32_t j = 0, first = 0; j < h.w; ++j, first += k)
+                err |= decode_pow2<V>(src[j], dc_log2b(c), min(k, nb - first), h.y, dst + first);
+            } else {
+              err |= decode_block_lane<V>(src, h.w, nb, c, h.z + 1, h.y, dst);
+            }
+          }
+        }
+      } else {
+        const uint32_t G = sh.G, nseg = nblk * G;
+        for (uint32_t seg = warp; seg < nseg; seg += NCW) {
+          const uint32_t b = seg / G, part = seg % G;
+          const uint4 h = H[b];
+          const uint32_t nb = min(L, nv - b * L);
+          V* dst = ob + (size_t)b * L;
+          const uint32_t k = (h.x == CODEC_BASIC && h.z != 0) ? k_of(bc, (uint64_t)h.z + 1) : 1u;
+          const uint32_t e = check_block_hdr(h, nb, sh.width, k);
+          err |= e;
+          if (e) continue;
+          if (h.x == CODEC_CONSTANT) {
+            const uint32_t lo = min(nb, part * sh.Lp), hi = min(nb, lo + sh.Lp);
+            for (uint32_t j = lo + lane; j < hi; j += 32) dst[j] = (V)h.y;
+          } else {
+            const DecConst c = dconst_of(bc, (uint64_t)h.z + 1);
+            const uint64_t* src = PAY + OFF[b];
+            uint32_t done = 0;
+            if (sizeof(V) == 2 && ((L * 2) & 15) == 0) {
+              uint8_t* blk = reinterpret_cast<uint8_t*>(dst);
+              const uint32_t Bu = h.z + 1;
+              switch (k) {
+#define POLY_UK(KK)                                                                                     \
+  case KK:                                                                                              \
+    err |= unpack_block_k<KK>(src, nb, c, Bu, h.y, part * 32 + lane, 32 * G, blk, &done);               \
+    break;
+                POLY_FOR_EACH_K16(POLY_UK)
+#undef POLY_UK
+                default:
+                  break;
+              }
+            }
+            for (uint32_t j = done + part * 32 + lane; j < h.w; j += 32 * G) {
+              const uint32_t first = j * k;
+              err |= decode_any<V>(src[j], c, h.z, min(k, nb - first), h.y, dst + first);
+            }
+          }
+        }
+      }
+    } else if (ctid == 0) {
+      err |= terr;
+    }
+    if (bst) fence_proxy_async_smem();
+    cons_bar();
+    uint8_t* og = a.out + v0 * sh.vb;
+    const uint32_t bytes = nv * sh.vb;
+    if (ctid == 0) {
+      __threadfence_block();
+      C.ring_tail = rend;  // the tile's payload words are consumed
+      mbar_arrive(&C.empty_in[s]);
+    }
+    if (bst) {
+      if (ctid == 0) {
+        const uint32_t b16 = bytes & ~15u;
+        if (b16) {
+          bulk_s2g(og, ob8, b16);
+          bulk_commit();
+        }
+        for (uint32_t j = b16; j < bytes; ++j) og[j] = ob8[j];
+      }
+    } else {
+      uint32_t done = 0;
+      if ((reinterpret_cast<uintptr_t>(og) & 15) == 0) {
+        const uint32_t n16 = bytes >> 4;
+        for (uint32_t j = ctid; j < n16; j += PC)
+          reinterpret_cast<uint4*>(og)[j] = reinterpret_cast<const uint4*>(ob8)[j];
+        done = n16 << 4;
+      }
+      for (uint32_t j = done + ctid; j < bytes; j += PC) og[j] = ob8[j];
+    }
+  }
+  if (a.bulk && !(a.debug & 4) && ctid == 0) bulk_wait_all<0>();
+  err = __reduce_or_sync(0xffffffffu, err);
+  if (lane == 0 && err) atomicOr(a.status_out, err);
+}
+
+}  // namespace polyk

@@ -17,6 +17,7 @@
 //          (WB blocks per unit); lane l owns words l, l+32, ... (contiguous).
 #pragma once
 #include "poly_common.cuh"
+#include "poly_word.cuh"
 
 namespace polyk {
 
@@ -65,14 +66,6 @@ __device__ __forceinline__ uint64_t warp_lookback(uint64_t* status, uint64_t uni
   const uint64_t p = lookback(status, unit);
   if ((threadIdx.x & 31) == 0) st_relaxed_u64(status + unit, FLAG_PRE | ((p + total) & VAL_MASK));
   return p;
-}
-
-// ceil(n / k) for n < 2^24, 1 <= k <= 64, without an integer divide.
-__device__ __forceinline__ uint32_t ceil_div_small(uint32_t n, uint32_t k) {
-  uint32_t q = (uint32_t)__fmul_rz((float)(n + k - 1), __frcp_rn((float)k));
-  if (q * k > n + k - 1) --q;
-  if ((q + 1) * k <= n + k - 1) ++q;
-  return q;
 }
 
 // Copy nbytes from global g to this warp's smem slice s (16-byte vectors when
@@ -125,206 +118,8 @@ __device__ __forceinline__ void warp_words_in(uint64_t* s, const uint64_t* g, ui
   for (; i < cnt; i += 32) s[i] = ldg_nc_u64(g + i);
 }
 
-// min / max of n values at s.
-template <typename V>
-__device__ __forceinline__ void block_minmax(const V* s, uint32_t n, uint32_t& mn, uint32_t& mx) {
-  if (sizeof(V) == 2 && (reinterpret_cast<uintptr_t>(s) & 3) == 0 && n >= 2) {
-    const uint32_t* w = reinterpret_cast<const uint32_t*>(s);
-    const uint32_t nw = n >> 1;
-    uint32_t a = w[0], b = w[0];
-    uint32_t i = 1;
-#pragma unroll 4
-    for (; i + 1 < nw; i += 2) {
-      const uint32_t x = w[i], y = w[i + 1];
-      a = __vimin3_u16x2(a, x, y);
-      b = __vimax3_u16x2(b, x, y);
-    }
-    if (i < nw) {
-      a = __vminu2(a, w[i]);
-      b = __vmaxu2(b, w[i]);
-    }
-    mn = min(a & 0xffffu, a >> 16);
-    mx = max(b & 0xffffu, b >> 16);
-    if (n & 1) {
-      const uint32_t x = (uint32_t)s[n - 1];
-      mn = min(mn, x);
-      mx = max(mx, x);
-    }
-  } else {
-    mn = 0xffffffffu;
-    mx = 0u;
-#pragma unroll 4
-    for (uint32_t i = 0; i < n; ++i) {
-      const uint32_t x = (uint32_t)s[i];
-      mn = min(mn, x);
-      mx = max(mx, x);
-    }
-  }
-}
-
-// ------------------------------------------------------------------ pack (a5)
-// Horner of Eq. 2 over 32-bit chunks of h digits:
-// s = sum_q c_q D^q, D = B^h, each chunk c_q < B^h <= 2^32 evaluated with
-// 32-bit multiply-adds, chunks combined top-down with 64x32 multiply-adds.
-// Requires B <= 2^32 - 1 (B = 2^32 goes through pack_word_b32).
-template <typename V>
-__device__ __forceinline__ uint32_t chunk32(const V* v, uint32_t len, uint32_t B, uint32_t vmin) {
-  uint32_t c = 0;
-#pragma unroll 4
-  for (int i = (int)len - 1; i >= 0; --i) c = c * B + ((uint32_t)v[i] - vmin);
-  return c;
-}
-
-template <typename V>
-__device__ __forceinline__ uint64_t pack_word(const V* v, uint32_t m, uint32_t B, uint32_t h, uint32_t D,
-                                              uint32_t vmin) {
-  // chunks from the top: the top one holds r = m - (nch-1) h digits
-  const uint32_t nch = m <= h ? 1u : (m <= 2 * h ? 2u : 3u);
-  const uint32_t r = m - (nch - 1) * h;
-  uint64_t s = chunk32<V>(v + (nch - 1) * h, r, B, vmin);
-  for (int q = (int)nch - 2; q >= 0; --q) {
-    const uint32_t c = chunk32<V>(v + q * h, h, B, vmin);
-    if (D == 0)  // D = 2^32 (B = 2^j, j | 32)
-      s = (s << 32) | c;
-    else
-      s = s * D + c;
-  }
-  return s;
-}
-
-template <typename V>
-__device__ __forceinline__ uint64_t pack_word_b32(const V* v, uint32_t m, uint32_t vmin) {
-  uint64_t s = 0;
-  for (int i = (int)m - 1; i >= 0; --i) s = (s << 32) | (uint32_t)((uint32_t)v[i] - vmin);
-  return s;
-}
-
-// Per-block packing parameters.
-struct PackParams {
-  uint32_t B, h, D, k;
-};
-__device__ __forceinline__ PackParams pack_params(uint32_t bm1) {
-  PackParams p;
-  p.B = bm1 + 1;  // wraps to 0 for B = 2^32 (handled by pack_word_b32)
-  capacity_kh((uint64_t)bm1 + 1, p.k, p.h);
-  uint64_t D = 1;
-  for (uint32_t i = 0; i < p.h; ++i) D *= (uint64_t)bm1 + 1;
-  p.D = (uint32_t)D;  // 0 iff D = 2^32
-  return p;
-}
-
-template <typename V>
-__device__ __forceinline__ uint64_t pack_any(const V* v, uint32_t m, const PackParams& p, uint32_t vmin) {
-  if (p.B == 0) return pack_word_b32<V>(v, m, vmin);
-  return pack_word<V>(v, m, p.B, p.h, p.D, vmin);
-}
-
-// ------------------------------------------------------------------ unpack (a8)
-// Word -> digits, most significant first, through the binary fraction
-// f in [s 2^64 / B^k, (s+1) 2^64 / B^k):
-//   f = floor(s R / 2^96) + 1,  R = ceil(2^160 / B^k);
-//   64-bit step: (d, f) = (floor(f B / 2^64), f B mod 2^64);
-//   after k - t32 digits the top 32 bits + 1 are an exact 32-bit fraction for
-//   the last t32 digits: (d, g) = (floor(g B / 2^32), g B mod 2^32).
-template <typename V>
-__device__ __forceinline__ uint32_t decode_frac(uint64_t s, const DecConst& c, uint32_t B, uint32_t m,
-                                                uint32_t vmin, V* out) {
-  if (s >= c.Bk) return POLY_ST_RESIDUE;
-  const uint64_t hi1 = __umul64hi(s, c.Rl);
-  const uint64_t lo2 = s * c.Rh;
-  const uint64_t hi2 = __umul64hi(s, c.Rh);
-  const uint64_t mid = lo2 + hi1;
-  const uint64_t f = ((hi2 + (mid < lo2 ? 1ull : 0ull)) << 32) + (mid >> 32) + 1;
-  uint32_t f0 = (uint32_t)f, f1 = (uint32_t)(f >> 32);
-  const int k = (int)dc_k(c), t = (int)dc_t32(c), mm = (int)m;
-  uint32_t extra = 0;
-  int i = k - 1;
-  const int za = max(t, mm);
-  for (; i >= za; --i) {  // 64-bit steps, digits that must be zero
-    const uint64_t t0 = (uint64_t)f0 * B;
-    const uint64_t t1 = (uint64_t)f1 * B + (uint32_t)(t0 >> 32);
-    extra |= (uint32_t)(t1 >> 32);
-    f1 = (uint32_t)t1;
-    f0 = (uint32_t)t0;
-  }
-#pragma unroll 2
-  for (; i >= t; --i) {  // 64-bit steps, output digits
-    const uint64_t t0 = (uint64_t)f0 * B;
-    const uint64_t t1 = (uint64_t)f1 * B + (uint32_t)(t0 >> 32);
-    out[i] = (V)(vmin + (uint32_t)(t1 >> 32));
-    f1 = (uint32_t)t1;
-    f0 = (uint32_t)t0;
-  }
-  uint32_t g = f1 + 1;
-  for (; i >= mm; --i) {  // 32-bit steps, digits that must be zero
-    const uint64_t p = (uint64_t)g * B;
-    extra |= (uint32_t)(p >> 32);
-    g = (uint32_t)p;
-  }
-#pragma unroll 4
-  for (; i >= 0; --i) {  // 32-bit steps, output digits
-    const uint64_t p = (uint64_t)g * B;
-    out[i] = (V)(vmin + (uint32_t)(p >> 32));
-    g = (uint32_t)p;
-  }
-  return extra ? POLY_ST_RESIDUE : 0u;
-}
-
-template <typename V>
-__device__ __forceinline__ uint32_t decode_pow2(uint64_t s, uint32_t j, uint32_t m, uint32_t vmin, V* out) {
-  const uint64_t mask = (1ull << j) - 1;  // j <= 32
-#pragma unroll 4
-  for (uint32_t i = 0; i < m; ++i) out[i] = (V)(vmin + (uint32_t)((s >> (i * j)) & mask));
-  return (m * j < 64 && (s >> (m * j)) != 0) ? POLY_ST_RESIDUE : 0u;
-}
-
-template <typename V>
-__device__ __forceinline__ uint32_t decode_any(uint64_t s, const DecConst& c, uint32_t bm1, uint32_t m,
-                                               uint32_t vmin, V* out) {
-  const uint32_t j = dc_log2b(c);
-  if (j) return decode_pow2<V>(s, j, m, vmin, out);
-  return decode_frac<V>(s, c, bm1 + 1, m, vmin, out);
-}
-
-// Block-header validation (a9) without an integer divide: n_words must be
-// ceil(n_b / k), i.e. (n_words - 1) k < n_b <= n_words k.
-__device__ __forceinline__ uint32_t check_block_hdr(uint4 h, uint32_t nb, uint32_t width, uint32_t k) {
-  const uint64_t vmax_allowed = (width == 16) ? 0xffffull : 0xffffffffull;
-  if (h.x == CODEC_CONSTANT) {
-    uint32_t e = 0;
-    if (h.z != 0 || h.w != 0) e |= POLY_ST_NWORDS;
-    if ((uint64_t)h.y > vmax_allowed) e |= POLY_ST_OVERFLOW;
-    return e;
-  }
-  if (h.x != CODEC_BASIC) return POLY_ST_BAD_CODEC;
-  if (h.z == 0 || (uint64_t)h.y + h.z > vmax_allowed) return POLY_ST_OVERFLOW;
-  if (h.w == 0 || (uint64_t)(h.w - 1) * k >= nb || (uint64_t)h.w * k < nb) return POLY_ST_NWORDS;
-  return 0;
-}
-
 __device__ __forceinline__ void write_global_header_w(uint8_t* out, const WarpShape& sh, uint64_t pw) {
-  uint4 h0, h1;
-  h0.x = 0x43594c50u;  // "PLYC"
-  h0.y = 2u | (sh.width << 16);
-  h0.z = (uint32_t)sh.n;
-  h0.w = (uint32_t)(sh.n >> 32);
-  h1.x = sh.block_len;
-  h1.y = (uint32_t)sh.n_blocks;
-  h1.z = (uint32_t)(pw * 8);
-  h1.w = (uint32_t)((pw * 8) >> 32);
-  reinterpret_cast<uint4*>(out)[0] = h0;
-  reinterpret_cast<uint4*>(out)[1] = h1;
-}
-
-// inclusive warp scan
-__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  return x;
+  write_global_header_f(out, sh.width, sh.n, sh.block_len, sh.n_blocks, pw);
 }
 
 // ======================================================================
