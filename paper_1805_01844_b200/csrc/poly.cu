@@ -53,6 +53,13 @@ void build_tables() {
       }
       if ((B & (B - 1)) == 0) {
         while ((1ull << log2b) != B) ++log2b;
+        // exact fraction: R = 2^(160 - kj), Wmax = B^k - 1, t32 = h = floor(32 / j)
+        const uint32_t kj = k * log2b;
+        const u128 R = ((u128)1) << (160 - kj);
+        c.Rl = (uint64_t)R;
+        c.Rh = (uint64_t)(R >> 64);
+        c.Wmax = (uint64_t)(p - 1);
+        t32 = std::min(k, 32u / log2b);
       } else {
         const uint64_t D = (uint64_t)p;  // B^k < 2^64 for non-powers of two
         u128 rem = 0, r = 0;
@@ -65,7 +72,7 @@ void build_tables() {
           }
         }
         r += 1;  // ceil: the remainder of 2^160 / D is nonzero
-        c.Bk = D;
+        c.Wmax = D - 1;
         c.Rl = (uint64_t)r;
         c.Rh = (uint64_t)(r >> 64);
         const u128 lim96 = ((u128)1) << 96;

@@ -24,13 +24,14 @@ constexpr uint32_t CODEC_CONSTANT = 1;
 constexpr uint32_t CODEC_BASIC = 2;
 
 // Per-base constants.  k = max{k : B^k <= 2^64} (Eq. 1,
-// reading R2) and h = max{h : B^h <= 2^32} (32-bit chunk length).  For a
-// non-power-of-two base: Bk = B^k < 2^64 and R = ceil(2^160 / B^k) < 2^128,
-// split R = Rh * 2^64 + Rl; t32 = the number of trailing digits of a word
-// that may be extracted with a 32-bit fraction (Sec. 5.3).  For B = 2^j the
-// decoder uses shifts and only k and log2b are meaningful.
+// reading R2) and h = max{h : B^h <= 2^32} (32-bit chunk length).  The
+// decoder's binary fraction of a word s < B^k is f = floor(s R / 2^96) + add:
+//   non-power-of-two B: R = ceil(2^160 / B^k) (< 2^128), add = 1;
+//   B = 2^j:            R = 2^(160 - kj) (exact),      add = 0.
+// Wmax = B^k - 1 is the largest valid word; t32 = the number of trailing
+// digits of a word that may be extracted with a 32-bit fraction (Sec. 5.3).
 struct __align__(16) DecConst {
-  uint64_t Bk;
+  uint64_t Wmax;
   uint64_t Rl;
   uint64_t Rh;
   uint32_t meta;  // k | log2b << 8 | t32 << 16 | h << 24
@@ -39,6 +40,7 @@ struct __align__(16) DecConst {
 __device__ __forceinline__ uint32_t dc_k(const DecConst& c) { return c.meta & 0xffu; }
 __device__ __forceinline__ uint32_t dc_log2b(const DecConst& c) { return (c.meta >> 8) & 0xffu; }
 __device__ __forceinline__ uint32_t dc_t32(const DecConst& c) { return (c.meta >> 16) & 0xffu; }
+__device__ __forceinline__ uint32_t dc_add(const DecConst& c) { return ((c.meta >> 8) & 0xffu) ? 0u : 1u; }
 
 // Filled once per device by poly_init (host computes them with exact 128-bit
 // integer arithmetic).  g_ktab[B] = k | h << 8.
@@ -84,16 +86,22 @@ __device__ __noinline__ DecConst dec_const_slow(uint64_t B) {
   DecConst c;
   const uint32_t k = B <= 2642245ull ? 3u : 2u;
   const uint32_t log2b = ((B & (B - 1)) == 0) ? (uint32_t)(63 - __clzll(B)) : 0u;
-  c.Bk = 0; c.Rl = 0; c.Rh = 0; c.pad = 0;
+  c.Wmax = 0; c.Rl = 0; c.Rh = 0; c.pad = 0;
   uint32_t t32 = 0;
   if (!log2b) {
     uint64_t p = 1;
     for (uint32_t i = 0; i < k; ++i) p *= B;
-    c.Bk = p;
+    c.Wmax = p - 1;
     recip160(p, c.Rl, c.Rh);
     // t32 <= h = 1: one trailing 32-bit digit iff 2^32 B^k + B^k + 2^64 B <= 2^96
     const unsigned __int128 lhs = ((unsigned __int128)p << 32) + p + ((unsigned __int128)B << 64);
     if (lhs <= ((unsigned __int128)1 << 96)) t32 = 1;
+  } else {  // B = 2^j, 17 <= j <= 32: exact fraction, R = 2^(160 - kj)
+    const uint32_t kj = k * log2b;
+    c.Wmax = kj >= 64 ? ~0ull : ((1ull << kj) - 1);
+    const uint32_t e = 160 - kj;  // 96 .. 109
+    c.Rh = 1ull << (e - 64);
+    t32 = 32 / log2b;
   }
   c.meta = k | (log2b << 8) | (t32 << 16) | (1u << 24);
   return c;

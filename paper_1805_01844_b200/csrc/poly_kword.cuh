@@ -162,7 +162,7 @@ __device__ __forceinline__ uint32_t unpack_group(const uint64_t* src, uint32_t g
       for (int i = 0; i < K; ++i) d[i] = (uint32_t)(s >> (i * j)) & (B - 1);
       if (K * j < 64 && (s >> (K * j)) != 0) err = POLY_ST_RESIDUE;
     } else {
-      if (s >= dc.Bk) err = POLY_ST_RESIDUE;
+      if (s > dc.Wmax) err = POLY_ST_RESIDUE;
       const uint64_t hi1 = __umul64hi(s, dc.Rl);
       const uint64_t lo2 = s * dc.Rh;
       const uint64_t hi2 = __umul64hi(s, dc.Rh);

@@ -35,7 +35,8 @@ constexpr int PC = NCW * 32;       // consumer threads
 constexpr int PT = PC + 96;        // + producer, writer and header-sum warps
 constexpr int W_PROD = NCW;        // warp index of the producer / header issuer
 constexpr int W_WRIT = NCW + 1;    // warp index of the writer / look-back warp
-constexpr int W_HSUM = NCW + 2;    // decompress: header-sum warp (compress: idle)
+constexpr int W_HSUM = NCW + 2;    // decompress: header-sum warp (compress: 2nd writer if NWRITERS = 2)
+constexpr int NWRITERS = 1;        // compress writer warps
 constexpr int MAXS = 8;            // max ring stages
 constexpr int BPT_MAX = 2;         // map 0: blocks per consumer thread
 constexpr uint32_t PIPE_MAX_BLOCK = 32768;  // bytes per block handled here
@@ -91,9 +92,11 @@ struct __align__(16) PipeCtl {
   uint32_t rec_off[MAXR];
   uint32_t cur_off;         // compress: ring offset of the tile being packed
   uint64_t payload_words;
-  volatile uint64_t ring_tail;  // ring bytes released (compress: by the writer; decompress: by the consumers)
+  volatile uint64_t ring_tail;  // ring bytes released (compress: by the writers; decompress: by the consumers)
+  volatile uint32_t wdone;      // compress: records completed, in order
   uint32_t hdr_err, pad;
   uint32_t scan[2][NCW];
+  uint32_t nwL[68];          // compress map 0: ceil(L / k) for k = 1..64
   uint32_t smin[256], smax[256];                        // map 1: partial min / max per segment
   uint32_t bvmin[256], bbm1[256], bnw[256], boff[256];  // map 1: per-block results
 };
@@ -186,7 +189,7 @@ __device__ __forceinline__ uint32_t cons_scan(uint32_t x, uint32_t* total, uint3
 // (k | log2b << 8 | t32 << 16 | h << 24).
 struct BaseCache {
   uint32_t* meta;
-  uint64_t* Bk;  // decompress: B^k
+  uint64_t* Bk;  // decompress: Wmax = B^k - 1
   uint64_t* Rl;  // decompress: ceil(2^160 / B^k), low / high 64 bits
   uint64_t* Rh;
   uint64_t* D;   // compress: B^h
@@ -220,7 +223,7 @@ __device__ __forceinline__ void cache_fill(const BaseCache& c, bool dec) {
     const DecConst d = g_dtab[B];
     c.meta[B] = d.meta;
     if (dec) {
-      c.Bk[B] = d.Bk;
+      c.Bk[B] = d.Wmax;
       c.Rl[B] = d.Rl;
       c.Rh[B] = d.Rh;
     } else {
@@ -263,7 +266,7 @@ __device__ __forceinline__ uint32_t kh_of16(const BaseCache& c, uint32_t B) {
 __device__ __forceinline__ DecConst dconst_of(const BaseCache& c, uint64_t B) {
   if (B <= CACHE_B) {
     DecConst d;
-    d.Bk = c.Bk[B];
+    d.Wmax = c.Bk[B];
     d.Rl = c.Rl[B];
     d.Rh = c.Rh[B];
     d.meta = c.meta[B];
@@ -348,11 +351,13 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_pipe(PipeArgs a) {
       mbar_init(&C.rec_empty[r], 1);
     }
     C.ring_tail = 0;
+    C.wdone = 0;
     mbar_fence_init();
   }
   cache_fill(bc, false);
+  if (MAP == 0)
+    for (uint32_t k = tid; k < 68; k += PT) C.nwL[k] = k ? (uint32_t)((sh.Le + k - 1) / k) : 0u;
   __syncthreads();
-  if (warp == W_HSUM) return;
 
   if (warp == W_PROD) {
     // ---------------------------------------------------------- producer
@@ -394,9 +399,11 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_pipe(PipeArgs a) {
   }
 
   uint64_t* pay_g = reinterpret_cast<uint64_t*>(a.out + 32 + 16 * sh.n_blocks);
-  if (warp == W_WRIT) {
-    // ---------------------------------------------------------- writer
-    for (uint32_t i = 0;; ++i) {
+  if (warp >= W_WRIT && warp < W_WRIT + NWRITERS) {
+    // ---------------------------------------------------------- writers
+    // NWRITERS writer warps take records round robin (look-backs overlap);
+    // ring space is released strictly in record order.
+    for (uint32_t i = (uint32_t)(warp - W_WRIT);; i += NWRITERS) {
       const uint32_t r = i % MAXR, ph = (i / MAXR) & 1u;
       mbar_wait(&C.rec_full[r], ph);
       const uint64_t t = C.rec_t[r];
@@ -425,13 +432,18 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_pipe(PipeArgs a) {
       }
       __syncwarp();
       if (lane == 0) {
+        while (C.wdone != i) __nanosleep(32);
         __threadfence_block();
         C.ring_tail = C.rec_end[r];
+        C.wdone = i + 1;
         mbar_arrive(&C.rec_empty[r]);
       }
+      __syncwarp();
     }
     return;
   }
+
+  if (warp >= NCW) return;  // spare warp (NWRITERS = 1)
 
   // ------------------------------------------------------------ consumers
   const int ctid = tid;  // 0 .. PC-1
@@ -442,11 +454,15 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_pipe(PipeArgs a) {
        s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0), r = (r + 1) % MAXR, rph ^= (r == 0)) {
     mbar_wait(&C.full_in[s], ph);
     const uint64_t t = C.tkt[s];
-    if (t == TILE_NONE) {
+    if (t == TILE_NONE) {  // one end marker per writer warp
       if (ctid == 0) {
-        mbar_wait(&C.rec_empty[r], rph ^ 1u);
-        C.rec_t[r] = TILE_NONE;
-        mbar_arrive(&C.rec_full[r]);
+        for (int e = 0; e < NWRITERS; ++e) {
+          mbar_wait(&C.rec_empty[r], rph ^ 1u);
+          C.rec_t[r] = TILE_NONE;
+          mbar_arrive(&C.rec_full[r]);
+          r = (r + 1) % MAXR;
+          rph ^= (r == 0);
+        }
       }
       break;
     }
@@ -484,7 +500,7 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_pipe(PipeArgs a) {
             bm1[q] = mx - mn;
             if (mx != mn) {
               kk[q] = sizeof(V) == 2 ? kh_of16(bc, mx - mn + 1) : k_of(bc, (uint64_t)(mx - mn) + 1);
-              nw[q] = ceil_div_small(nb, kk[q] & 0xffu);
+              nw[q] = nb == L ? C.nwL[kk[q] & 0xffu] : ceil_div_small(nb, kk[q] & 0xffu);
             }
             hdr_g[b0 + b] = make_uint4(mx == mn ? CODEC_CONSTANT : CODEC_BASIC, mn, mx - mn, nw[q]);
           }
@@ -697,26 +713,15 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_pipe(PipeArgs a) {
       }
       uint8_t* st = smem + sh.o_in + (size_t)s * sh.in_stride;
       const uint4* H = reinterpret_cast<const uint4*>(st);
-      uint32_t* OFF = reinterpret_cast<uint32_t*>(st + sh.o_off);
+      uint32_t* OFF = reinterpret_cast<uint32_t*>(smem + sh.o_in + (size_t)s * sh.in_stride + sh.o_off);
       const uint64_t b0 = t * sh.TB;
       const uint32_t nblk = (uint32_t)min((uint64_t)sh.TB, sh.n_blocks - b0);
-      const uint32_t q = (nblk + 31) >> 5, lo = min(nblk, lane * q), hi = min(nblk, lo + q);
-      uint64_t sum = 0;
-      for (uint32_t b = lo; b < hi; ++b) sum += H[b].w;
-      uint64_t inc = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-      }
-      const uint64_t W = __shfl_sync(0xffffffffu, inc, 31);
-      if (W <= sh.words_cap) {
-        uint32_t ex = (uint32_t)(inc - sum);
-        for (uint32_t b = lo; b < hi; ++b) {
-          OFF[b] = ex;
-          ex += H[b].w;
-        }
-      }
+      // lane-strided, bank-conflict-free reads of the n_words fields; the
+      // in-tile offsets are scanned by the consumers
+      const uint32_t* Hw = reinterpret_cast<const uint32_t*>(H) + 3;
+      uint64_t part = 0;
+      for (uint32_t b = lane; b < nblk; b += 32) part += Hw[4 * b];
+      const uint64_t W = warp_sum_u64(part);
       __syncwarp();
       if (lane == 0) {
         st_relaxed_u64(a.status + t, (t == 0 ? FLAG_PRE : FLAG_AGG) | (W & VAL_MASK));
@@ -751,7 +756,7 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_pipe(PipeArgs a) {
         if (lane == 0) st_relaxed_u64(a.status + t, FLAG_PRE | ((P + W) & VAL_MASK));
       }
       uint32_t e = 0;
-      uint64_t wl = W;
+      uint64_t wl = (a.debug & 16) ? 0 : W;
       if (W > sh.words_cap || P + W > pw) {
         e = POLY_ST_LENGTH;
         wl = 0;
@@ -806,7 +811,7 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_pipe(PipeArgs a) {
     if (t == TILE_NONE) break;
     const uint8_t* st = smem + sh.o_in + (size_t)s * sh.in_stride;
     const uint4* H = reinterpret_cast<const uint4*>(st);
-    const uint32_t* OFF = reinterpret_cast<const uint32_t*>(st + sh.o_off);
+    uint32_t* OFF = reinterpret_cast<uint32_t*>(smem + sh.o_in + (size_t)s * sh.in_stride + sh.o_off);
     const uint64_t* PAY = reinterpret_cast<const uint64_t*>(ring + C.ring_off[s]) + (C.P[s] & 1);
     const uint32_t terr = C.err[s];
     const uint64_t rend = C.ring_end[s];
@@ -817,7 +822,22 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_pipe(PipeArgs a) {
     const uint64_t v0 = b0 * sh.Le;
     const uint32_t nv = (uint32_t)(min(sh.n, v0 + (uint64_t)sh.TB * sh.Le) - v0);
     const bool bst = a.bulk && !(a.debug & 4);  // TMA bulk store of the tile (else coalesced STG)
+    const bool nostore = (a.debug & 8) != 0;
     if (bst && ctid == 0) bulk_wait_read<1>();  // staging buffer s2 is free again
+    // in-tile word offsets of the blocks (a7): CTA scan of the n_words fields
+    // (a tile with W > words_cap was rejected by the look-back warp)
+    {
+      const uint32_t* Hw = reinterpret_cast<const uint32_t*>(H) + 3;
+      uint32_t base = 0;
+      for (uint32_t b0s = 0; b0s < nblk; b0s += PC) {
+        const uint32_t b = b0s + ctid;
+        const uint32_t x = (b < nblk && terr == 0) ? Hw[4 * b] : 0u;
+        uint32_t tot;
+        const uint32_t ex = cons_scan(x, &tot, C.scan[(b0s / PC) & 1]);
+        if (b < nblk) OFF[b] = base + ex;
+        base += tot;
+      }
+    }
     cons_bar();
     if (terr == 0 && !(a.debug & 1)) {
       if (MAP == 0) {
@@ -836,9 +856,9 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_pipe(PipeArgs a) {
           } else {
             const DecConst c = dconst_of(bc, (uint64_t)h.z + 1);
             const uint64_t* src = PAY + OFF[b];
-            if (dc_log2b(c)) {
+            if (dc_log2b(c) == 32) {  // B = 2^32 (u32 only) does not fit the 32-bit multiplier
               for (uint32_t j = 0, first = 0; j < h.w; ++j, first += k)
-                err |= decode_pow2<V>(src[j], dc_log2b(c), min(k, nb - first), h.y, dst + first);
+                err |= decode_pow2<V>(src[j], 32, min(k, nb - first), h.y, dst + first);
             } else {
               err |= decode_block_lane<V>(src, h.w, nb, c, h.z + 1, h.y, dst);
             }
@@ -895,7 +915,8 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_pipe(PipeArgs a) {
       C.ring_tail = rend;  // the tile's payload words are consumed
       mbar_arrive(&C.empty_in[s]);
     }
-    if (bst) {
+    if (nostore) {
+    } else if (bst) {
       if (ctid == 0) {
         const uint32_t b16 = bytes & ~15u;
         if (b16) {

@@ -14,21 +14,25 @@ __device__ __forceinline__ uint32_t ceil_div_small(uint32_t n, uint32_t k) {
   return q;
 }
 
-// min / max of n values at s.
+// min / max of n values at s (one thread).  u16 at a 4-byte boundary: packed
+// u16x2 min/max over 32-bit words, four words per step.
 template <typename V>
 __device__ __forceinline__ void block_minmax(const V* s, uint32_t n, uint32_t& mn, uint32_t& mx) {
-  if (sizeof(V) == 2 && (reinterpret_cast<uintptr_t>(s) & 3) == 0 && n >= 2) {
+  if (sizeof(V) == 2 && (reinterpret_cast<uintptr_t>(s) & 3) == 0) {
     const uint32_t* w = reinterpret_cast<const uint32_t*>(s);
     const uint32_t nw = n >> 1;
-    uint32_t a = w[0], b = w[0];
-    uint32_t i = 1;
-#pragma unroll 4
-    for (; i + 1 < nw; i += 2) {
-      const uint32_t x = w[i], y = w[i + 1];
-      a = __vimin3_u16x2(a, x, y);
-      b = __vimax3_u16x2(b, x, y);
+    uint32_t a = 0xffffffffu, b = 0u;
+    uint32_t i = 0;
+#pragma unroll 1
+    for (; i + 4 <= nw; i += 4) {
+      const uint32_t x0 = w[i], x1 = w[i + 1], x2 = w[i + 2], x3 = w[i + 3];
+      a = __vimin3_u16x2(a, x0, x1);
+      b = __vimax3_u16x2(b, x0, x1);
+      a = __vimin3_u16x2(a, x2, x3);
+      b = __vimax3_u16x2(b, x2, x3);
     }
-    if (i < nw) {
+#pragma unroll 1
+    for (; i < nw; ++i) {
       a = __vminu2(a, w[i]);
       b = __vmaxu2(b, w[i]);
     }
@@ -212,37 +216,52 @@ __device__ __forceinline__ void pack_block_lane16(const uint16_t* v, uint32_t nb
   const uint32_t corr = vmin * G;
   const bool odd = k != 2 * h;
   const uint64_t DD = D * D;
-  // full words
-  const uint32_t nfull = nb / k;
+  const uint32_t nfull = (nw * k == nb) ? nw : nw - 1;  // nw = ceil(nb / k)
+  const uint32_t B2 = B * B;                            // B < 2^16 unless B = 2^16 (then B2 = 0, h = 2)
+#pragma unroll 1
   for (uint32_t j = 0; j < nfull; ++j) {
-    const uint16_t* w = v + j * k;
+    // two chains, two digits per step: c = c B^2 + (w[i] B + w[i-1])
+    const uint16_t* pl = v + j * k + h;  // one past the top digit of the lo chunk
+    const uint16_t* ph = pl + h;
     uint32_t lo = 0, hi = 0;
-    int i = (int)h - 1;
-    for (; i >= 1; i -= 2) {
-      lo = lo * B + w[i];
-      hi = hi * B + w[h + i];
-      lo = lo * B + w[i - 1];
-      hi = hi * B + w[h + i - 1];
+    if (h & 1) {
+      --pl;
+      --ph;
+      lo = *pl;
+      hi = *ph;
     }
-    if (i == 0) {
-      lo = lo * B + w[0];
-      hi = hi * B + w[h];
+#pragma unroll 1
+    for (uint32_t i = h >> 1; i > 0; --i) {
+      pl -= 2;
+      ph -= 2;
+      lo = lo * B2 + (pl[1] * B + pl[0]);
+      hi = hi * B2 + (ph[1] * B + ph[0]);
     }
     uint64_t s = (uint64_t)(hi - corr) * D + (lo - corr);
-    if (odd) s += (uint64_t)(w[2 * h] - vmin) * DD;
+    if (odd) s += (uint64_t)(v[j * k + 2 * h] - vmin) * DD;
     dst[j] = s;
   }
-  if (nfull < nw) {  // the top word: m < k digits, the rest are 0
-    const uint32_t base = nfull * k, m = nb - base;
-    const uint16_t* w = v + base;
+  if (nfull < nw) {  // the top word: m < k <= 2h + 1 digits, the missing ones are 0
+    const uint32_t m = nb - nfull * k;
+    const uint16_t* w = v + nfull * k;
+    const uint32_t ml = min(m, h), mh = m > h ? m - h : 0u;  // lo / hi chain lengths
+    const uint32_t vB1 = vmin * (B + 1);                     // a digit pair's share of vmin
     uint32_t lo = 0, hi = 0;
-    for (int i = (int)h - 1; i >= 0; --i) {
-      lo = lo * B + ((uint32_t)i < m ? (uint32_t)w[i] : vmin);
-      hi = hi * B + (h + (uint32_t)i < m ? (uint32_t)w[h + i] : vmin);
+    const uint16_t* pl = w + ml;
+    const uint16_t* ph = w + h + mh;
+    if (ml & 1) lo = (uint32_t)*--pl - vmin;
+    if (mh & 1) hi = (uint32_t)*--ph - vmin;
+#pragma unroll 1
+    for (uint32_t i = ml >> 1; i > 0; --i) {
+      pl -= 2;
+      lo = lo * B2 + (pl[1] * B + pl[0] - vB1);
     }
-    uint64_t s = (uint64_t)(hi - corr) * D + (lo - corr);
-    if (odd && 2 * h < m) s += (uint64_t)(w[2 * h] - vmin) * DD;
-    dst[nfull] = s;
+#pragma unroll 1
+    for (uint32_t i = mh >> 1; i > 0; --i) {
+      ph -= 2;
+      hi = hi * B2 + (ph[1] * B + ph[0] - vB1);
+    }
+    dst[nfull] = (uint64_t)hi * D + lo;
   }
 }
 
@@ -254,15 +273,16 @@ template <typename V>
 __device__ __forceinline__ uint32_t decode_pair(uint64_t sa, uint64_t sb, const DecConst& c, uint32_t B,
                                                 uint32_t ma, uint32_t mb, uint32_t vmin, V* oa, V* ob) {
   uint32_t extra = 0;
-  if (sa >= c.Bk || sb >= c.Bk) return POLY_ST_RESIDUE;
+  if (sa > c.Wmax || sb > c.Wmax) return POLY_ST_RESIDUE;
+  const uint32_t add = dc_add(c);
   uint64_t fa, fb;
   {
     const uint64_t hi1 = __umul64hi(sa, c.Rl), lo2 = sa * c.Rh, hi2 = __umul64hi(sa, c.Rh), mid = lo2 + hi1;
-    fa = ((hi2 + (mid < lo2 ? 1ull : 0ull)) << 32) + (mid >> 32) + 1;
+    fa = ((hi2 + (mid < lo2 ? 1ull : 0ull)) << 32) + (mid >> 32) + add;
   }
   {
     const uint64_t hi1 = __umul64hi(sb, c.Rl), lo2 = sb * c.Rh, hi2 = __umul64hi(sb, c.Rh), mid = lo2 + hi1;
-    fb = ((hi2 + (mid < lo2 ? 1ull : 0ull)) << 32) + (mid >> 32) + 1;
+    fb = ((hi2 + (mid < lo2 ? 1ull : 0ull)) << 32) + (mid >> 32) + add;
   }
   uint32_t a0 = (uint32_t)fa, a1 = (uint32_t)(fa >> 32), b0 = (uint32_t)fb, b1 = (uint32_t)(fb >> 32);
   const int k = (int)dc_k(c), t = (int)dc_t32(c);
@@ -278,7 +298,7 @@ __device__ __forceinline__ uint32_t decode_pair(uint64_t sa, uint64_t sb, const 
     if ((uint32_t)i < ma) oa[i] = (V)(vmin + da); else extra |= da;
     if ((uint32_t)i < mb) ob[i] = (V)(vmin + db); else extra |= db;
   }
-  uint32_t ga = a1 + 1, gb = b1 + 1;
+  uint32_t ga = a1 + add, gb = b1 + add;
   for (; i >= 0; --i) {
     const uint64_t pa = (uint64_t)ga * B, pb = (uint64_t)gb * B;
     const uint32_t da = (uint32_t)(pa >> 32), db = (uint32_t)(pb >> 32);
@@ -290,18 +310,59 @@ __device__ __forceinline__ uint32_t decode_pair(uint64_t sa, uint64_t sb, const 
   return extra ? POLY_ST_RESIDUE : 0u;
 }
 
-// All words of one block, one thread, two words at a time (non-power-of-two B).
+// Three words in lock step (three independent chains); see decode_pair.
+template <typename V>
+__device__ __forceinline__ uint32_t decode_triple(uint64_t sa, uint64_t sb, uint64_t sc, const DecConst& c,
+                                                  uint32_t B, uint32_t ma, uint32_t mb, uint32_t mc, uint32_t vmin,
+                                                  V* oa, V* ob, V* oc) {
+  uint32_t extra = 0;
+  if (sa > c.Wmax || sb > c.Wmax || sc > c.Wmax) return POLY_ST_RESIDUE;
+  const uint32_t add = dc_add(c);
+  uint64_t f[3];
+  const uint64_t sv[3] = {sa, sb, sc};
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const uint64_t hi1 = __umul64hi(sv[q], c.Rl), lo2 = sv[q] * c.Rh, hi2 = __umul64hi(sv[q], c.Rh);
+    const uint64_t mid = lo2 + hi1;
+    f[q] = ((hi2 + (mid < lo2 ? 1ull : 0ull)) << 32) + (mid >> 32) + add;
+  }
+  uint32_t a0 = (uint32_t)f[0], a1 = (uint32_t)(f[0] >> 32), b0 = (uint32_t)f[1], b1 = (uint32_t)(f[1] >> 32);
+  uint32_t c0 = (uint32_t)f[2], c1 = (uint32_t)(f[2] >> 32);
+  const int k = (int)dc_k(c), t = (int)dc_t32(c);
+  int i = k - 1;
+  for (; i >= t; --i) {
+    const uint64_t ta = (uint64_t)a0 * B, tb = (uint64_t)b0 * B, tc = (uint64_t)c0 * B;
+    const uint64_t ua = (uint64_t)a1 * B + (uint32_t)(ta >> 32), ub = (uint64_t)b1 * B + (uint32_t)(tb >> 32);
+    const uint64_t uc = (uint64_t)c1 * B + (uint32_t)(tc >> 32);
+    const uint32_t da = (uint32_t)(ua >> 32), db = (uint32_t)(ub >> 32), dd = (uint32_t)(uc >> 32);
+    a1 = (uint32_t)ua; a0 = (uint32_t)ta;
+    b1 = (uint32_t)ub; b0 = (uint32_t)tb;
+    c1 = (uint32_t)uc; c0 = (uint32_t)tc;
+    if ((uint32_t)i < ma) oa[i] = (V)(vmin + da); else extra |= da;
+    if ((uint32_t)i < mb) ob[i] = (V)(vmin + db); else extra |= db;
+    if ((uint32_t)i < mc) oc[i] = (V)(vmin + dd); else extra |= dd;
+  }
+  uint32_t ga = a1 + add, gb = b1 + add, gc = c1 + add;
+  for (; i >= 0; --i) {
+    const uint64_t pa = (uint64_t)ga * B, pb = (uint64_t)gb * B, pc = (uint64_t)gc * B;
+    const uint32_t da = (uint32_t)(pa >> 32), db = (uint32_t)(pb >> 32), dd = (uint32_t)(pc >> 32);
+    ga = (uint32_t)pa; gb = (uint32_t)pb; gc = (uint32_t)pc;
+    if ((uint32_t)i < ma) oa[i] = (V)(vmin + da); else extra |= da;
+    if ((uint32_t)i < mb) ob[i] = (V)(vmin + db); else extra |= db;
+    if ((uint32_t)i < mc) oc[i] = (V)(vmin + dd); else extra |= dd;
+  }
+  return extra ? POLY_ST_RESIDUE : 0u;
+}
+
+// All words of one block, one thread (B < 2^32).
 template <typename V>
 __device__ __forceinline__ uint32_t decode_block_lane(const uint64_t* src, uint32_t nw, uint32_t nb,
                                                       const DecConst& c, uint32_t B, uint32_t vmin, V* out) {
   const uint32_t k = dc_k(c);
   uint32_t err = 0;
-  uint32_t j = 0;
-  for (; j + 1 < nw; j += 2) {
-    const uint32_t fa = j * k, fb = fa + k;
-    err |= decode_pair<V>(src[j], src[j + 1], c, B, min(k, nb - fa), min(k, nb - fb), vmin, out + fa, out + fb);
-  }
-  if (j < nw) err |= decode_frac<V>(src[j], c, B, min(k, nb - j * k), vmin, out + j * k);
+#pragma unroll 1
+  for (uint32_t j = 0, first = 0; j < nw; ++j, first += k)
+    err |= decode_frac<V>(src[j], c, B, min(k, nb - first), vmin, out + first);
   return err;
 }
 
@@ -312,47 +373,72 @@ __device__ __forceinline__ uint32_t decode_block_lane(const uint64_t* src, uint3
 //   64-bit step: (d, f) = (floor(f B / 2^64), f B mod 2^64);
 //   after k - t32 digits the top 32 bits + 1 are an exact 32-bit fraction for
 //   the last t32 digits: (d, g) = (floor(g B / 2^32), g B mod 2^32).
+// One 64-bit fraction step (d, f) = (floor(f B / 2^64), f B mod 2^64), and
+// one 32-bit step (d, g) = (floor(g B / 2^32), g B mod 2^32).
+__device__ __forceinline__ uint32_t frac_step64(uint32_t& f0, uint32_t& f1, uint32_t B) {
+  uint32_t n0, n1, c, d;
+  asm("mul.lo.u32 %0, %4, %6;\n\t"
+      "mul.hi.u32 %1, %4, %6;\n\t"
+      "mad.lo.cc.u32 %2, %5, %6, %1;\n\t"
+      "madc.hi.u32 %3, %5, %6, 0;"
+      : "=&r"(n0), "=&r"(c), "=&r"(n1), "=r"(d)  // early clobber: outputs are written before the inputs are all read
+      : "r"(f0), "r"(f1), "r"(B));
+  f0 = n0;
+  f1 = n1;
+  return d;
+}
+__device__ __forceinline__ uint32_t frac_step32(uint32_t& g, uint32_t B) {
+  uint32_t lo, hi;
+  asm("mul.lo.u32 %0, %2, %3;\n\tmul.hi.u32 %1, %2, %3;" : "=&r"(lo), "=r"(hi) : "r"(g), "r"(B));
+  g = lo;
+  return hi;
+}
+
+// Word -> its m low digits (out[i] = vmin + digit i, i < m), most significant
+// first; digits m..k-1 must be 0.  Plain loops (two digits per iteration): the
+// loop trip counts are the only thing that differs between lanes.
 template <typename V>
 __device__ __forceinline__ uint32_t decode_frac(uint64_t s, const DecConst& c, uint32_t B, uint32_t m,
                                                 uint32_t vmin, V* out) {
-  if (s >= c.Bk) return POLY_ST_RESIDUE;
-  const uint64_t hi1 = __umul64hi(s, c.Rl);
-  const uint64_t lo2 = s * c.Rh;
-  const uint64_t hi2 = __umul64hi(s, c.Rh);
-  const uint64_t mid = lo2 + hi1;
-  const uint64_t f = ((hi2 + (mid < lo2 ? 1ull : 0ull)) << 32) + (mid >> 32) + 1;
+  if (s > c.Wmax) return POLY_ST_RESIDUE;
+  const uint32_t add = dc_add(c);
+  const uint64_t hi1 = __umul64hi(s, c.Rl), lo2 = s * c.Rh, hi2 = __umul64hi(s, c.Rh), mid = lo2 + hi1;
+  const uint64_t f = ((hi2 + (mid < lo2 ? 1ull : 0ull)) << 32) + (mid >> 32) + add;
   uint32_t f0 = (uint32_t)f, f1 = (uint32_t)(f >> 32);
   const int k = (int)dc_k(c), t = (int)dc_t32(c), mm = (int)m;
   uint32_t extra = 0;
   int i = k - 1;
-  const int za = max(t, mm);
-  for (; i >= za; --i) {  // 64-bit steps, digits that must be zero
-    const uint64_t t0 = (uint64_t)f0 * B;
-    const uint64_t t1 = (uint64_t)f1 * B + (uint32_t)(t0 >> 32);
-    extra |= (uint32_t)(t1 >> 32);
-    f1 = (uint32_t)t1;
-    f0 = (uint32_t)t0;
+  if (mm < k) {  // the top word of a block: its top k - m digits are 0
+    const int za = max(t, mm);
+#pragma unroll 1
+    for (; i >= za; --i) extra |= frac_step64(f0, f1, B);
   }
-#pragma unroll 2
-  for (; i >= t; --i) {  // 64-bit steps, output digits
-    const uint64_t t0 = (uint64_t)f0 * B;
-    const uint64_t t1 = (uint64_t)f1 * B + (uint32_t)(t0 >> 32);
-    out[i] = (V)(vmin + (uint32_t)(t1 >> 32));
-    f1 = (uint32_t)t1;
-    f0 = (uint32_t)t0;
+  V* o = out + i;
+#pragma unroll 1
+  for (; i >= t + 1; i -= 2, o -= 2) {
+    const uint32_t d1 = frac_step64(f0, f1, B);
+    const uint32_t d0 = frac_step64(f0, f1, B);
+    o[0] = (V)(vmin + d1);
+    o[-1] = (V)(vmin + d0);
   }
-  uint32_t g = f1 + 1;
-  for (; i >= mm; --i) {  // 32-bit steps, digits that must be zero
-    const uint64_t p = (uint64_t)g * B;
-    extra |= (uint32_t)(p >> 32);
-    g = (uint32_t)p;
+  if (i >= t) {
+    o[0] = (V)(vmin + frac_step64(f0, f1, B));
+    --i;
+    --o;
   }
-#pragma unroll 4
-  for (; i >= 0; --i) {  // 32-bit steps, output digits
-    const uint64_t p = (uint64_t)g * B;
-    out[i] = (V)(vmin + (uint32_t)(p >> 32));
-    g = (uint32_t)p;
+  uint32_t g = f1 + add;
+  if (i >= mm) {
+#pragma unroll 1
+    for (; i >= mm; --i, --o) extra |= frac_step32(g, B);
   }
+#pragma unroll 1
+  for (; i >= 1; i -= 2, o -= 2) {
+    const uint32_t d1 = frac_step32(g, B);
+    const uint32_t d0 = frac_step32(g, B);
+    o[0] = (V)(vmin + d1);
+    o[-1] = (V)(vmin + d0);
+  }
+  if (i == 0) o[0] = (V)(vmin + frac_step32(g, B));
   return extra ? POLY_ST_RESIDUE : 0u;
 }
 
