@@ -9,9 +9,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpolycomp.so")
+# Tuning variants (A/B timing only): extra -D flags and a different file name.
+VARIANT_FLAGS = os.environ.get("POLY_VARIANT_FLAGS", "").split()
+if VARIANT_FLAGS:
+    LIB = os.path.join(HERE, "libpolycomp_%s.so" % os.environ.get("POLY_VARIANT_NAME", "variant"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 SOURCES = ["poly.cu"]
-DEPS = ["poly.cu", "poly_common.cuh", "poly_compress.cuh", "poly_decompress.cuh", "poly_warp.cuh", "poly_word.cuh", "poly_pipe.cuh", "poly_kword.cuh"]
+DEPS = ["poly.cu", "poly_common.cuh", "poly_compress.cuh", "poly_decompress.cuh", "poly_word.cuh", "poly_pipe.cuh", "poly_kword.cuh", "poly_large.cuh"]
 
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -34,7 +38,7 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    cmd = [NVCC] + FLAGS + ["-I", os.path.join(ROOT, "include")] + \
+    cmd = [NVCC] + FLAGS + VARIANT_FLAGS + ["-I", os.path.join(ROOT, "include")] + \
         [os.path.join(CSRC, s) for s in SOURCES] + ["-o", LIB + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -42,8 +46,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed building libpolycomp.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    with open(os.path.join(HERE, "ptxas_report.txt"), "w") as f:
-        f.write(r.stderr)
+    if not VARIANT_FLAGS:
+        with open(os.path.join(HERE, "ptxas_report.txt"), "w") as f:
+            f.write(r.stderr)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -9,14 +9,14 @@
 #include "poly_common.cuh"
 #include "poly_compress.cuh"
 #include "poly_decompress.cuh"
-#include "poly_warp.cuh"
 #include "poly_pipe.cuh"
+#include "poly_large.cuh"
 
 using namespace polyk;
 
 namespace {
 
-enum Regime { WARP = 0, LARGE = 1, PIPE = 2 };
+enum Regime { LARGE = 1, PIPE = 2, LARGE2 = 3 };
 
 constexpr int MAX_DEVICES = 64;
 std::mutex g_mu;
@@ -29,6 +29,7 @@ typedef unsigned __int128 u128;
 uint16_t h_ktab[KTAB_MAX + 1];
 DecConst h_dtab[KTAB_MAX + 1];
 bool h_tables_built = false;
+bool h_tables_bad = false;  // a Sec. 5.3 precondition failed (never expected)
 
 // k = max{k : B^k <= 2^64}, h = max{h : B^h <= 2^32}; for non-powers of two
 // B^k, R = ceil(2^160 / B^k) and t32 = max{t <= min(k, h) :
@@ -62,6 +63,8 @@ void build_tables() {
         t32 = std::min(k, 32u / log2b);
       } else {
         const uint64_t D = (uint64_t)p;  // B^k < 2^64 for non-powers of two
+        // the fraction error bound needs B^k < 2^64 - 2^32
+        if (word_ring - p <= ((u128)1 << 32)) h_tables_bad = true;
         u128 rem = 0, r = 0;
         for (int i = 160; i >= 0; --i) {
           rem = (rem << 1) | (i == 160 ? 1u : 0u);
@@ -108,22 +111,14 @@ poly_status_t ensure_init(int dev) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (g_ready[dev]) return POLY_OK;
   build_tables();
+  if (h_tables_bad) return POLY_ERR_CUDA;
   int cur = 0;
   if (cudaGetDevice(&cur) != cudaSuccess) return POLY_ERR_CUDA;
   if (cur != dev && cudaSetDevice(dev) != cudaSuccess) return POLY_ERR_CUDA;
   cudaError_t e = cudaMemcpyToSymbol(g_ktab, h_ktab, sizeof h_ktab);
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_dtab, h_dtab, sizeof h_dtab);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
-  const int wmax = WARPS * (2 * WT_MAX + 512);
-  set_smem_attr(poly_compress_warp<uint16_t, 0>, wmax);
-  set_smem_attr(poly_compress_warp<uint16_t, 1>, wmax);
-  set_smem_attr(poly_compress_warp<uint32_t, 0>, wmax);
-  set_smem_attr(poly_compress_warp<uint32_t, 1>, wmax);
-  set_smem_attr(poly_decompress_warp<uint16_t, 0>, wmax);
-  set_smem_attr(poly_decompress_warp<uint16_t, 1>, wmax);
-  set_smem_attr(poly_decompress_warp<uint32_t, 0>, wmax);
-  set_smem_attr(poly_decompress_warp<uint32_t, 1>, wmax);
-  const int pmax = 227 * 1024;
+  const int pmax = (POLY_CTAS == 1 ? 227 : 113) * 1024;
   set_smem_attr(poly_compress_pipe<uint16_t, 0>, pmax);
   set_smem_attr(poly_compress_pipe<uint16_t, 1>, pmax);
   set_smem_attr(poly_compress_pipe<uint32_t, 0>, pmax);
@@ -132,6 +127,10 @@ poly_status_t ensure_init(int dev) {
   set_smem_attr(poly_decompress_pipe<uint16_t, 1>, pmax);
   set_smem_attr(poly_decompress_pipe<uint32_t, 0>, pmax);
   set_smem_attr(poly_decompress_pipe<uint32_t, 1>, pmax);
+  set_smem_attr(poly_compress_large<uint16_t>, pmax);
+  set_smem_attr(poly_compress_large<uint32_t>, pmax);
+  set_smem_attr(poly_decompress_large<uint16_t>, pmax);
+  set_smem_attr(poly_decompress_large<uint32_t>, pmax);
   set_smem_attr(poly_compress_pack<uint16_t>, large_smem_pack<uint16_t>());
   set_smem_attr(poly_compress_pack<uint32_t>, large_smem_pack<uint32_t>());
   set_smem_attr(poly_decompress_unpack<uint16_t>, large_smem_unpack<uint16_t>());
@@ -147,8 +146,8 @@ poly_status_t ensure_init(int dev) {
 // arguments always give the same shape (the stream does not depend on it).
 constexpr uint32_t WT_TARGET = 4096;  // input bytes per warp unit (target)
 
-constexpr uint32_t PIPE_TILE_TARGET = 32768;  // value bytes per tile (target)
-constexpr uint32_t PIPE_SMEM_MAX = 227 * 1024;  // one CTA per SM
+constexpr uint32_t PIPE_TILE_TARGET = 32768 / POLY_CTAS;          // value bytes per tile (target)
+constexpr uint32_t PIPE_SMEM_MAX = (POLY_CTAS == 1 ? 227 : 113) * 1024;  // shared memory per CTA
 
 uint32_t r16(uint64_t x) { return (uint32_t)((x + 15) / 16 * 16); }
 
@@ -163,7 +162,7 @@ bool plan_pipe(const Shape& sh, PipeShape& ps, bool decomp) {
   ps.vb = sh.width / 8;
   const uint64_t bb = sh.Le * ps.vb;
   const uint64_t kmin = sh.width == 16 ? 4 : 2;
-  if (bb <= LANE_BLOCK_MAX) {
+  if (bb <= MAP0_MAX_BLOCK) {
     ps.map = 0;
     uint64_t bpt = PIPE_TILE_TARGET / (PC * bb);
     bpt = std::max<uint64_t>(1, std::min<uint64_t>(BPT_MAX, bpt));
@@ -218,10 +217,42 @@ bool plan_pipe(const Shape& sh, PipeShape& ps, bool decomp) {
   return ps.smem <= PIPE_SMEM_MAX;
 }
 
-bool plan(uint64_t n, uint32_t w, uint64_t block_size, Shape& sh, WarpShape& ws, Regime& rg) {
+// Large blocks, one CTA per block (poly_large.cuh): sub-tiles of 32 KiB plus a
+// halo, S stages; decompress adds two staging buffers of one sub-tile.
+constexpr uint64_t LARGE2_MIN_BLOCKS = 256;     // enough blocks to occupy every SM
+constexpr uint64_t LARGE2_MAX_BLOCK = 4 << 20;  // bytes: sweep 1 must find the block in L2
+bool plan_large(const Shape& sh, LargeShape& ls, bool decomp) {
+  memset(&ls, 0, sizeof ls);
+  ls.n = sh.n;
+  ls.Le = sh.Le;
+  ls.n_blocks = sh.n_blocks;
+  ls.block_len = sh.block_len;
+  ls.width = sh.width;
+  ls.vb = sh.width / 8;
+  ls.SV = 32768 / ls.vb;
+  ls.nsub = (uint32_t)((sh.Le + ls.SV - 1) / ls.SV);
+  const uint32_t ctl = (uint32_t)((sizeof(LargeCtl) + 127) / 128 * 128);
+  if (!decomp) {
+    ls.stage = r16((uint64_t)(ls.SV + LG_HALO) * ls.vb);
+    ls.S = 4;
+    ls.o_in = ctl;
+    ls.smem = ctl + ls.S * ls.stage;
+  } else {
+    const uint64_t kmin = sh.width == 16 ? 4 : 2;
+    ls.stage = r16(8ull * (ls.SV / kmin + 4));
+    const uint32_t outb = 2 * ls.SV * ls.vb;
+    ls.S = (uint32_t)std::min<uint64_t>(MAXS, (PIPE_SMEM_MAX - ctl - outb) / ls.stage);
+    if (ls.S < 2) return false;
+    ls.o_in = ctl;
+    ls.o_out = ctl + ls.S * ls.stage;
+    ls.smem = ls.o_out + outb;
+  }
+  return ls.smem <= PIPE_SMEM_MAX;
+}
+
+bool plan(uint64_t n, uint32_t w, uint64_t block_size, Shape& sh, Regime& rg) {
   if (n == 0 || (w != 16 && w != 32) || block_size >= (1ull << 32)) return false;
   memset(&sh, 0, sizeof sh);
-  memset(&ws, 0, sizeof ws);
   sh.n = n;
   sh.width = w;
   sh.block_len = (uint32_t)block_size;
@@ -230,9 +261,14 @@ bool plan(uint64_t n, uint32_t w, uint64_t block_size, Shape& sh, WarpShape& ws,
   if (sh.n_blocks >= (1ull << 32)) return false;
   const uint64_t bb = sh.Le * (w / 8);  // bytes per block
   PipeShape pc, pd;
+  LargeShape lc, ld;
   if (bb <= PIPE_MAX_BLOCK && plan_pipe(sh, pc, false) && plan_pipe(sh, pd, true)) {
     rg = PIPE;
     sh.n_chunks = pc.n_tiles;  // tiles (look-back units)
+  } else if (bb <= LARGE2_MAX_BLOCK && sh.n_blocks >= LARGE2_MIN_BLOCKS && plan_large(sh, lc, false) &&
+             plan_large(sh, ld, true)) {
+    rg = LARGE2;
+    sh.n_chunks = sh.n_blocks;  // blocks (look-back units)
   } else {
     rg = LARGE;
     sh.cpb = (sh.Le + CH_VALUES - 1) / CH_VALUES;
@@ -246,13 +282,11 @@ struct WsLayout {
   uint64_t status_off, bmin_off, bmax_off, woff_off, total;
 };
 
-WsLayout ws_layout(const Shape& sh, const WarpShape& ws, Regime rg) {
+WsLayout ws_layout(const Shape& sh, Regime rg) {
   WsLayout L;
   memset(&L, 0, sizeof L);
   L.status_off = 64;
-  if (rg == WARP) {
-    L.total = 64 + 8 * ws.n_units;
-  } else if (rg == PIPE) {
+  if (rg == PIPE || rg == LARGE2) {
     L.total = 64 + 8 * sh.n_chunks;
   } else {
     L.bmin_off = (64 + 8 * sh.n_stiles + 15) / 16 * 16;
@@ -274,23 +308,18 @@ int grid_for(uint64_t work, int dev) {
   return (int)std::min<uint64_t>(work, cap);
 }
 
-// Persistent grid for a warp-tile kernel: every resident CTA, capped by work.
-template <typename K>
-int warp_grid(K kernel, uint32_t smem, uint64_t units, int dev) {
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, WARPS * 32, smem) != cudaSuccess ||
-      per_sm < 1)
-    per_sm = 1;
-  const uint64_t cap = (uint64_t)(g_sms[dev] > 0 ? g_sms[dev] : 148) * per_sm;
-  const uint64_t need = (units + WARPS - 1) / WARPS;
-  return (int)std::max<uint64_t>(1, std::min<uint64_t>(cap, need));
-}
 
 // POLY_DEBUG (timing experiments only; the output is then wrong): bit 0 skips
 // the per-block compute, bit 1 the look-back.
 uint32_t debug_flags() {
   const char* e = getenv("POLY_DEBUG");
   return e ? (uint32_t)strtoul(e, nullptr, 0) : 0u;
+}
+// Look-back warps per CTA (1 or 2); POLY_LB overrides the default.
+uint32_t lb_warps(uint32_t dflt) {
+  const char* e = getenv("POLY_LB");
+  const uint32_t v = e ? (uint32_t)strtoul(e, nullptr, 0) : dflt;
+  return v == 2 ? 2u : 1u;
 }
 
 template <typename K>
@@ -336,18 +365,16 @@ uint64_t poly_max_compressed_bytes(uint64_t n, poly_dtype_t dt, uint64_t block_s
 
 uint64_t poly_workspace_bytes(uint64_t n, poly_dtype_t dt, uint64_t block_size) {
   Shape sh;
-  WarpShape ws;
   Regime rg;
-  if (!plan(n, (uint32_t)dt, block_size, sh, ws, rg)) return 0;
-  return ws_layout(sh, ws, rg).total;
+  if (!plan(n, (uint32_t)dt, block_size, sh, rg)) return 0;
+  return ws_layout(sh, rg).total;
 }
 
 int poly_launches_per_call(uint64_t n, poly_dtype_t dt, uint64_t block_size, int decompress) {
   Shape sh;
-  WarpShape ws;
   Regime rg;
-  if (!plan(n, (uint32_t)dt, block_size, sh, ws, rg)) return 0;
-  if (rg == WARP || rg == PIPE) return 1;
+  if (!plan(n, (uint32_t)dt, block_size, sh, rg)) return 0;
+  if (rg == PIPE || rg == LARGE2) return 1;
   return decompress ? 2 : 3;
 }
 
@@ -363,11 +390,10 @@ poly_status_t poly_compress(const void* d_in, uint64_t n, poly_dtype_t dt, uint6
   if ((reinterpret_cast<uintptr_t>(d_compressed_bytes) & 7) != 0) return POLY_ERR_INVALID_ARG;
   if ((reinterpret_cast<uintptr_t>(d_workspace) & 15) != 0) return POLY_ERR_INVALID_ARG;
   Shape sh;
-  WarpShape wsh;
   Regime rg;
-  if (!plan(n, (uint32_t)dt, block_size, sh, wsh, rg)) return POLY_ERR_INVALID_ARG;
+  if (!plan(n, (uint32_t)dt, block_size, sh, rg)) return POLY_ERR_INVALID_ARG;
   if (out_capacity < poly_max_compressed_bytes(n, dt, block_size)) return POLY_ERR_CAPACITY;
-  const WsLayout W = ws_layout(sh, wsh, rg);
+  const WsLayout W = ws_layout(sh, rg);
   if (workspace_bytes < W.total) return POLY_ERR_WORKSPACE;
   const int dev = current_device();
   poly_status_t st = ensure_init(dev);
@@ -383,7 +409,20 @@ poly_status_t poly_compress(const void* d_in, uint64_t n, poly_dtype_t dt, uint6
   a.ticket = reinterpret_cast<uint32_t*>(ws);
   a.status = reinterpret_cast<uint64_t*>(ws + W.status_off);
   a.sh = sh;
-  if (rg == PIPE) {
+  if (rg == LARGE2) {
+    cudaMemsetAsync(ws, 0, W.total, s);
+    LargeArgs la;
+    memset(&la, 0, sizeof la);
+    plan_large(sh, la.sh, false);
+    la.in = reinterpret_cast<const uint8_t*>(d_in);
+    la.out = a.out;
+    la.compressed_bytes = d_compressed_bytes;
+    la.status = a.status;
+    la.ticket = a.ticket;
+    la.bulk = ((reinterpret_cast<uintptr_t>(d_in) & 15) == 0 && (sh.Le * (dt / 8)) % 16 == 0) ? 1u : 0u;
+    auto k = dt == POLY_U16 ? poly_compress_large<uint16_t> : poly_compress_large<uint32_t>;
+    k<<<pipe_grid(k, la.sh.smem, sh.n_blocks, dev), PT, la.sh.smem, s>>>(la);
+  } else if (rg == PIPE) {
     cudaMemsetAsync(ws, 0, W.total, s);
     PipeArgs pa;
     memset(&pa, 0, sizeof pa);
@@ -395,23 +434,10 @@ poly_status_t poly_compress(const void* d_in, uint64_t n, poly_dtype_t dt, uint6
     pa.ticket = a.ticket;
     pa.bulk = ((reinterpret_cast<uintptr_t>(d_in) & 15) == 0 && pa.sh.tile_bytes % 16 == 0) ? 1u : 0u;
     pa.debug = debug_flags();
+    pa.nlb = lb_warps(1);
     auto k = dt == POLY_U16 ? (pa.sh.map == 0 ? poly_compress_pipe<uint16_t, 0> : poly_compress_pipe<uint16_t, 1>)
                             : (pa.sh.map == 0 ? poly_compress_pipe<uint32_t, 0> : poly_compress_pipe<uint32_t, 1>);
     k<<<pipe_grid(k, pa.sh.smem, pa.sh.n_tiles, dev), PT, pa.sh.smem, s>>>(pa);
-  } else if (rg == WARP) {
-    cudaMemsetAsync(ws, 0, W.total, s);
-    WarpArgs wa;
-    memset(&wa, 0, sizeof wa);
-    wa.in = reinterpret_cast<const uint8_t*>(d_in);
-    wa.out = a.out;
-    wa.compressed_bytes = d_compressed_bytes;
-    wa.status = a.status;
-    wa.ticket = a.ticket;
-    wa.sh = wsh;
-    const uint32_t smem = WARPS * wsh.slice;
-    auto k = dt == POLY_U16 ? (wsh.mode == 0 ? poly_compress_warp<uint16_t, 0> : poly_compress_warp<uint16_t, 1>)
-                            : (wsh.mode == 0 ? poly_compress_warp<uint32_t, 0> : poly_compress_warp<uint32_t, 1>);
-    k<<<warp_grid(k, smem, wsh.n_units, dev), WARPS * 32, smem, s>>>(wa);
   } else {
     a.bmin = reinterpret_cast<uint32_t*>(ws + W.bmin_off);
     a.bmax = reinterpret_cast<uint32_t*>(ws + W.bmax_off);
@@ -465,10 +491,9 @@ poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_
   if ((reinterpret_cast<uintptr_t>(d_out) % vb) != 0) return POLY_ERR_INVALID_ARG;
   if ((reinterpret_cast<uintptr_t>(d_workspace) & 15) != 0) return POLY_ERR_INVALID_ARG;
   Shape sh;
-  WarpShape wsh;
   Regime rg;
-  if (!plan(n, (uint32_t)dt, block_size, sh, wsh, rg)) return POLY_ERR_INVALID_ARG;
-  const WsLayout W = ws_layout(sh, wsh, rg);
+  if (!plan(n, (uint32_t)dt, block_size, sh, rg)) return POLY_ERR_INVALID_ARG;
+  const WsLayout W = ws_layout(sh, rg);
   if (workspace_bytes < W.total) return POLY_ERR_WORKSPACE;
   const int dev = current_device();
   poly_status_t st = ensure_init(dev);
@@ -486,7 +511,21 @@ poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_
   a.status = reinterpret_cast<uint64_t*>(ws + W.status_off);
   a.sh = sh;
   cudaMemsetAsync(d_status, 0, 4, s);
-  if (rg == PIPE) {
+  if (rg == LARGE2) {
+    cudaMemsetAsync(ws, 0, W.total, s);
+    LargeArgs la;
+    memset(&la, 0, sizeof la);
+    plan_large(sh, la.sh, true);
+    la.in = a.in;
+    la.out = reinterpret_cast<uint8_t*>(d_out);
+    la.in_bytes = compressed_bytes;
+    la.status_out = d_status;
+    la.status = a.status;
+    la.ticket = a.ticket;
+    la.bulk = ((reinterpret_cast<uintptr_t>(d_out) & 15) == 0 && (sh.Le * (dt / 8)) % 16 == 0) ? 1u : 0u;
+    auto k = dt == POLY_U16 ? poly_decompress_large<uint16_t> : poly_decompress_large<uint32_t>;
+    k<<<pipe_grid(k, la.sh.smem, sh.n_blocks, dev), PT, la.sh.smem, s>>>(la);
+  } else if (rg == PIPE) {
     cudaMemsetAsync(ws, 0, W.total, s);
     PipeArgs pa;
     memset(&pa, 0, sizeof pa);
@@ -499,26 +538,11 @@ poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_
     pa.ticket = a.ticket;
     pa.bulk = ((reinterpret_cast<uintptr_t>(d_out) & 15) == 0 && pa.sh.tile_bytes % 16 == 0) ? 1u : 0u;
     pa.debug = debug_flags();
+    pa.nlb = lb_warps(1);
     auto k = dt == POLY_U16
                  ? (pa.sh.map == 0 ? poly_decompress_pipe<uint16_t, 0> : poly_decompress_pipe<uint16_t, 1>)
                  : (pa.sh.map == 0 ? poly_decompress_pipe<uint32_t, 0> : poly_decompress_pipe<uint32_t, 1>);
     k<<<pipe_grid(k, pa.sh.smem, pa.sh.n_tiles, dev), PT, pa.sh.smem, s>>>(pa);
-  } else if (rg == WARP) {
-    cudaMemsetAsync(ws, 0, W.total, s);
-    WarpArgs wa;
-    memset(&wa, 0, sizeof wa);
-    wa.in = a.in;
-    wa.out = reinterpret_cast<uint8_t*>(d_out);
-    wa.in_bytes = compressed_bytes;
-    wa.status_out = d_status;
-    wa.status = a.status;
-    wa.ticket = a.ticket;
-    wa.sh = wsh;
-    const uint32_t smem = WARPS * wsh.slice;
-    auto k = dt == POLY_U16
-                 ? (wsh.mode == 0 ? poly_decompress_warp<uint16_t, 0> : poly_decompress_warp<uint16_t, 1>)
-                 : (wsh.mode == 0 ? poly_decompress_warp<uint32_t, 0> : poly_decompress_warp<uint32_t, 1>);
-    k<<<warp_grid(k, smem, wsh.n_units, dev), WARPS * 32, smem, s>>>(wa);
   } else {
     a.woff = reinterpret_cast<uint64_t*>(ws + W.woff_off);
     cudaMemsetAsync(ws, 0, W.bmin_off, s);

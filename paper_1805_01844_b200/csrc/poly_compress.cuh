@@ -3,7 +3,8 @@
 // Large-block regime (block_len * w > WT_MAX, e.g. cfg1 / cfg3): chunked
 // min/max with atomics (a2), a look-back scan over blocks for B, k, n_words,
 // headers and payload offsets (a3, a4, a6), then a chunked Horner pack pass
-// (a5).  Blocks up to WT_MAX bytes use the warp-tile kernels (poly_warp.cuh).
+// (a5).  Used for blocks the pipeline kernels do not take (few blocks larger
+// than 32 KiB, e.g. cfg1's single block); see poly.cu plan().
 #pragma once
 #include "poly_common.cuh"
 

@@ -9,7 +9,7 @@
 // multiply-adds per digit.  Power-of-two bases use shifts and masks.
 #pragma once
 #include "poly_common.cuh"
-#include "poly_warp.cuh"
+#include "poly_word.cuh"
 
 namespace polyk {
 

@@ -217,6 +217,19 @@ __device__ __forceinline__ uint32_t pack_block_k(const uint8_t* blk, uint32_t nb
   return ngroups * C::Q;
 }
 
+// Groups [gb, ge) of a block, lane-strided, by one warp; returns status bits.
+template <int K>
+__device__ __forceinline__ uint32_t unpack_groups_k(const uint64_t* src, uint32_t gb, uint32_t ge, const DecConst& dc,
+                                                    uint32_t B, uint32_t vmin, uint8_t* blk) {
+  uint32_t err = 0;
+  for (uint32_t g = gb + (threadIdx.x & 31); g < ge; g += 32) err |= unpack_group<K>(src, g, dc, B, vmin, blk);
+  return err;
+}
+template <int K>
+__host__ __device__ constexpr uint32_t kvals() { return (uint32_t)KCls<K>::VALS; }
+template <int K>
+__host__ __device__ constexpr uint32_t kq() { return (uint32_t)KCls<K>::Q; }
+
 template <int K>
 __device__ __forceinline__ uint32_t unpack_block_k(const uint64_t* src, uint32_t nb, const DecConst& dc, uint32_t B,
                                                    uint32_t vmin, uint32_t g0, uint32_t gstep, uint8_t* blk,

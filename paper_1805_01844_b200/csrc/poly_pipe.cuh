@@ -30,16 +30,26 @@
 
 namespace polyk {
 
-constexpr int NCW = 16;            // consumer warps
+#ifndef POLY_NCW
+#define POLY_NCW 16  // consumer warps per CTA
+#endif
+#ifndef POLY_CTAS
+#define POLY_CTAS 1  // CTAs per SM the shared-memory plan targets
+#endif
+constexpr int NCW = POLY_NCW;      // consumer warps
 constexpr int PC = NCW * 32;       // consumer threads
-constexpr int PT = PC + 96;        // + producer, writer and header-sum warps
+constexpr int PT = PC + 128;       // + producer, writer(s), header-sum and 2nd look-back warps
 constexpr int W_PROD = NCW;        // warp index of the producer / header issuer
 constexpr int W_WRIT = NCW + 1;    // warp index of the writer / look-back warp
-constexpr int W_HSUM = NCW + 2;    // decompress: header-sum warp (compress: 2nd writer if NWRITERS = 2)
+constexpr int W_HSUM = NCW + 2;    // decompress: header-sum warp (compress: 2nd writer)
+constexpr int W_LB2 = NCW + 3;     // decompress: 2nd look-back warp
 constexpr int NWRITERS = 1;        // compress writer warps
+// Look-back warps per CTA (compress writers / decompress look-back warps):
+// PipeArgs.nlb = 1 or 2 (host: POLY_LB env, default below).
 constexpr int MAXS = 8;            // max ring stages
 constexpr int BPT_MAX = 2;         // map 0: blocks per consumer thread
 constexpr uint32_t PIPE_MAX_BLOCK = 32768;  // bytes per block handled here
+constexpr uint32_t MAP0_MAX_BLOCK = 128;    // bytes per block for one consumer thread per block
 constexpr uint32_t CACHE_B = 512;  // shared-memory cache of per-base constants
 constexpr uint64_t TILE_NONE = ~0ull;
 constexpr int BAR_CONS = 1;        // named barrier id of the consumer warps
@@ -60,7 +70,11 @@ struct PipeShape {
   uint32_t o_off;       // decompress: offset of OFF[] inside a header stage (HDR at 0)
   uint32_t o_cache;     // offset of the base-constant cache
   uint32_t o_in, o_out; // offsets of the stages and the staging buffers
-  uint32_t o_ring, ring_bytes;  // decompress: payload ring
+  uint32_t o_ring, ring_bytes;  // decompress: payload ring; compress: word slots
+  uint32_t segcap;      // compress: worst-case words of one segment
+  uint32_t nslot;       // compress: records in flight (<= MAXR)
+  uint32_t slot_bytes;  // compress: bytes of each consumer warp's word ring
+  uint32_t pad3;
   uint32_t smem;        // dynamic shared memory bytes
 };
 
@@ -74,29 +88,37 @@ struct PipeArgs {
   uint32_t* ticket;
   uint32_t bulk;            // value array 16-byte aligned and tile_bytes % 16 == 0
   uint32_t debug;           // timing experiments only (POLY_DEBUG): 1 skip compute, 2 skip look-back
+  uint32_t nlb;             // look-back warps (1 or 2)
+  uint32_t pad2;
   PipeShape sh;
 };
 
-constexpr int MAXR = 8;            // compress: records in flight (consumers -> writer)
+constexpr int MAXR = 8;            // compress: word slots (tiles between consumers and writer)
+constexpr int MAXSEG = 256;        // segments per tile (map 0: warp groups of 32 blocks; map 1: blocks)
 
 struct __align__(16) PipeCtl {
-  uint64_t full_in[MAXS], empty_in[MAXS], hbar[MAXS], aggr[MAXS];
-  uint64_t rec_full[MAXR], rec_empty[MAXR];
+  uint64_t full_in[MAXS], empty_in[MAXS];    // stage filled (1 + tx) / released (NCW warps)
+  uint64_t hbar[MAXS], aggr[MAXS];           // decompress: headers landed / aggregate published
+  uint64_t rec_full[MAXR];    // compress: record ready for the writer
   uint64_t tkt[MAXS];       // ticket of the tile held by each stage
   uint64_t W[MAXS];         // decompress: payload words of the stage's tile
   uint64_t P[MAXS];         // decompress: payload word prefix of the stage's tile
   uint64_t ring_end[MAXS];  // decompress: ring position after the stage's payload
   uint32_t ring_off[MAXS];  // decompress: byte offset of the stage's payload in the ring
   uint32_t err[MAXS];       // decompress: tile-level status bits
+  uint32_t done_cnt[MAXS];  // decompress: warps done with the stage
   uint64_t rec_t[MAXR], rec_W[MAXR], rec_end[MAXR];  // compress: staged tiles
+  uint64_t rec_empty[MAXR];
   uint32_t rec_off[MAXR];
   uint32_t cur_off;         // compress: ring offset of the tile being packed
-  uint64_t payload_words;
-  volatile uint64_t ring_tail;  // ring bytes released (compress: by the writers; decompress: by the consumers)
-  volatile uint32_t wdone;      // compress: records completed, in order
-  uint32_t hdr_err, pad;
+  volatile uint32_t wdone;  // compress: records completed, in order
   uint32_t scan[2][NCW];
-  uint32_t nwL[68];          // compress map 0: ceil(L / k) for k = 1..64
+  uint64_t payload_words;
+  volatile uint64_t ring_tail;  // decompress: ring bytes released by the consumers
+  volatile uint32_t lb_seq;     // decompress: next stage to take ring space
+  uint64_t ring_head;           // decompress: ring bytes handed out
+  uint32_t hdr_err, pad;
+  uint32_t nwL[68];             // compress map 0: ceil(L / k) for k = 1..64
   uint32_t smin[256], smax[256];                        // map 1: partial min / max per segment
   uint32_t bvmin[256], bbm1[256], bnw[256], boff[256];  // map 1: per-block results
 };
@@ -120,14 +142,27 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t tx) {
 }
 // Wait for the phase with the given parity to complete.  The suspend-time hint
 // parks the thread in the barrier unit instead of spinning on issue slots.
+#ifndef POLY_SUSPEND_NS
+#define POLY_SUSPEND_NS 0x989680u
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if POLY_SUSPEND_NS > 0
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(0x989680u)
+      "r"(parity), "r"((uint32_t)POLY_SUSPEND_NS)
       : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+#endif
 }
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
@@ -167,6 +202,15 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void cons_bar() { asm volatile("bar.sync %0, %1;" ::"n"(BAR_CONS), "n"(PC) : "memory"); }
+// Named barrier of the G consecutive warps that share one block (map 1, G > 1).
+__device__ __forceinline__ void group_bar(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t x, uint32_t* total) {
+  const uint32_t inc = warp_incl_scan(x);
+  *total = __shfl_sync(0xffffffffu, inc, 31);
+  return inc - x;
+}
 
 // Exclusive scan of x over the PC consumer threads; *total = sum.  `buf`
 // alternates between calls (a call's barrier protects the buffer of the
@@ -188,6 +232,7 @@ __device__ __forceinline__ uint32_t cons_scan(uint32_t x, uint32_t* total, uint3
 // lanes with nearby bases hit different banks).  cmeta = DecConst.meta
 // (k | log2b << 8 | t32 << 16 | h << 24).
 struct BaseCache {
+  uint64_t* P;   // decompress map 0: B^(k - m_top(L)), 0 if the top word of an L-block is full
   uint32_t* meta;
   uint64_t* Bk;  // decompress: Wmax = B^k - 1
   uint64_t* Rl;  // decompress: ceil(2^160 / B^k), low / high 64 bits
@@ -203,10 +248,12 @@ __device__ __forceinline__ BaseCache cache_at(uint8_t* base, bool dec) {
     c.Bk = p;
     c.Rl = p + (CACHE_B + 1);
     c.Rh = p + 2 * (CACHE_B + 1);
-    c.meta = reinterpret_cast<uint32_t*>(p + 3 * (CACHE_B + 1));
+    c.P = p + 3 * (CACHE_B + 1);
+    c.meta = reinterpret_cast<uint32_t*>(p + 4 * (CACHE_B + 1));
     c.D = nullptr;
     c.G = nullptr;
   } else {
+    c.P = nullptr;
     c.D = p;
     c.meta = reinterpret_cast<uint32_t*>(p + (CACHE_B + 1));
     c.G = c.meta + (CACHE_B + 1);
@@ -215,10 +262,10 @@ __device__ __forceinline__ BaseCache cache_at(uint8_t* base, bool dec) {
   return c;
 }
 __host__ __device__ constexpr uint32_t cache_bytes(bool dec) {
-  return dec ? (uint32_t)(3 * 8 * (CACHE_B + 1) + 4 * (CACHE_B + 1) + 15) / 16 * 16
+  return dec ? (uint32_t)(4 * 8 * (CACHE_B + 1) + 4 * (CACHE_B + 1) + 15) / 16 * 16
              : (uint32_t)(8 * (CACHE_B + 1) + 8 * (CACHE_B + 1) + 15) / 16 * 16;
 }
-__device__ __forceinline__ void cache_fill(const BaseCache& c, bool dec) {
+__device__ __forceinline__ void cache_fill(const BaseCache& c, bool dec, uint64_t L = 0) {
   for (uint32_t B = threadIdx.x; B <= CACHE_B; B += blockDim.x) {
     const DecConst d = g_dtab[B];
     c.meta[B] = d.meta;
@@ -226,6 +273,16 @@ __device__ __forceinline__ void cache_fill(const BaseCache& c, bool dec) {
       c.Bk[B] = d.Wmax;
       c.Rl[B] = d.Rl;
       c.Rh[B] = d.Rh;
+      uint64_t P = 0;
+      const uint32_t k = d.meta & 0xffu;
+      if (B >= 2 && L != 0 && k != 0) {
+        const uint64_t mt = L - ((L + k - 1) / k - 1) * k;  // digits of an L-block's top word
+        if (mt < k) {
+          P = 1;
+          for (uint32_t i = 0; i < k - mt; ++i) P *= B;
+        }
+      }
+      c.P[B] = P;
     } else {
       const uint32_t h = d.meta >> 24;
       uint64_t D = 1;
@@ -646,7 +703,7 @@ __device__ __forceinline__ uint32_t check_global_header_p(const PipeArgs& a, uin
 }
 
 template <typename V, int MAP>
-__global__ void __launch_bounds__(PT, 1) poly_decompress_pipe(PipeArgs a) {
+__global__ void __launch_bounds__(PT, POLY_CTAS) poly_decompress_pipe(PipeArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   PipeCtl& C = *reinterpret_cast<PipeCtl*>(smem);
   const PipeShape& sh = a.sh;
@@ -659,15 +716,18 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_pipe(PipeArgs a) {
       mbar_init(&C.hbar[s], 1);
       mbar_init(&C.aggr[s], 1);
       mbar_init(&C.full_in[s], 1);
-      mbar_init(&C.empty_in[s], 1);
+      mbar_init(&C.empty_in[s], NCW);
+      C.done_cnt[s] = 0;
     }
     mbar_fence_init();
     uint64_t pw;
     C.hdr_err = check_global_header_p(a, &pw);
     C.payload_words = pw;
     C.ring_tail = 0;
+    C.lb_seq = 0;
+    C.ring_head = 0;
   }
-  cache_fill(bc, true);
+  cache_fill(bc, true, MAP == 0 ? sh.Le : 0);
   __syncthreads();
   if (C.hdr_err) {  // same verdict in every CTA: nothing is decoded, no look-back
     if (blockIdx.x == 0 && tid == 0) atomicOr(a.status_out, C.hdr_err);
@@ -679,13 +739,19 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_pipe(PipeArgs a) {
   if (warp == W_PROD) {
     // ---------------------------------------------------------- header issuer
     if (lane != 0) return;
+    uint32_t nend = 0;  // end markers emitted (one per look-back warp)
     for (uint32_t i = 0, s = 0, ph = 0;; ++i) {
       mbar_wait(&C.empty_in[s], ph ^ 1u);
-      const uint64_t t = atomicAdd(a.ticket, 1u);
+      const uint64_t t = nend ? sh.n_tiles : atomicAdd(a.ticket, 1u);
       if (t >= sh.n_tiles) {
         C.tkt[s] = TILE_NONE;
         mbar_arrive(&C.hbar[s]);
-        break;
+        if (++nend == a.nlb) break;
+        if (++s == S) {
+          s = 0;
+          ph ^= 1u;
+        }
+        continue;
       }
       C.tkt[s] = t;
       const uint64_t b0 = t * sh.TB;
@@ -704,24 +770,43 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_pipe(PipeArgs a) {
     // ---------------------------------------------------------- header sum
     // Publishes each tile's aggregate as soon as its headers land (a7), and
     // the in-tile word offsets of its blocks.
+    uint32_t nend = 0;
     for (uint32_t s = 0, ph = 0;;) {
       mbar_wait(&C.hbar[s], ph);
       const uint64_t t = C.tkt[s];
       if (t == TILE_NONE) {
         if (lane == 0) mbar_arrive(&C.aggr[s]);
-        break;
+        if (++nend == a.nlb) break;
+        if (++s == S) {
+          s = 0;
+          ph ^= 1u;
+        }
+        continue;
       }
       uint8_t* st = smem + sh.o_in + (size_t)s * sh.in_stride;
       const uint4* H = reinterpret_cast<const uint4*>(st);
       uint32_t* OFF = reinterpret_cast<uint32_t*>(smem + sh.o_in + (size_t)s * sh.in_stride + sh.o_off);
       const uint64_t b0 = t * sh.TB;
       const uint32_t nblk = (uint32_t)min((uint64_t)sh.TB, sh.n_blocks - b0);
-      // lane-strided, bank-conflict-free reads of the n_words fields; the
-      // in-tile offsets are scanned by the consumers
+      // rounds of 32 blocks, lane-strided (bank-conflict free).  map 0: round r is
+      // warp group r of the consumers -> OFF[r] = words before the group; map 1:
+      // OFF[b] = words before block b.  (Offsets of a tile with W > words_cap
+      // are garbage; the look-back warp rejects such a tile.)
       const uint32_t* Hw = reinterpret_cast<const uint32_t*>(H) + 3;
-      uint64_t part = 0;
-      for (uint32_t b = lane; b < nblk; b += 32) part += Hw[4 * b];
-      const uint64_t W = warp_sum_u64(part);
+      uint64_t W = 0;
+      for (uint32_t r0 = 0, rr = 0; r0 < nblk; r0 += 32, ++rr) {
+        const uint32_t b = r0 + lane;
+        const uint32_t x = b < nblk ? Hw[4 * b] : 0u;
+        if (MAP == 0) {
+          if (lane == 0) OFF[rr] = (uint32_t)W;
+          W += warp_sum_u64(x);
+        } else {
+          uint32_t tot;
+          const uint32_t ex = warp_excl_scan(x, &tot);
+          if (b < nblk) OFF[b] = (uint32_t)W + ex;
+          W += warp_sum_u64(x);
+        }
+      }
       __syncwarp();
       if (lane == 0) {
         st_relaxed_u64(a.status + t, (t == 0 ? FLAG_PRE : FLAG_AGG) | (W & VAL_MASK));
@@ -736,11 +821,14 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_pipe(PipeArgs a) {
     return;
   }
 
-  if (warp == W_WRIT) {
+  if (warp == W_WRIT || (warp == W_LB2 && a.nlb == 2)) {
     // ---------------------------------------------------------- look-back + payload loader
+    // nlb warps take stages round robin, so nlb look-backs are in flight; ring
+    // space is handed out strictly in stage order (C.lb_seq).
     const uint64_t pw = C.payload_words;
-    uint64_t head = 0;  // ring bytes handed out (lane 0's copy is authoritative)
-    for (uint32_t s = 0, ph = 0;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0)) {
+    const uint32_t nlb = a.nlb;
+    for (uint32_t i = (warp == W_WRIT) ? 0u : 1u;; i += nlb) {
+      const uint32_t s = i % S, ph = (i / S) & 1u;
       mbar_wait(&C.aggr[s], ph);
       const uint64_t t = C.tkt[s];
       if (t == TILE_NONE) {
@@ -766,6 +854,9 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_pipe(PipeArgs a) {
       if (lane == 0) {
         C.P[s] = P;
         C.err[s] = e;
+        while (C.lb_seq != i) __nanosleep(32);  // in-order ring allocation
+        __threadfence_block();
+        uint64_t head = C.ring_head;
         if (wl) {
           const uint64_t a0 = P & ~1ull, hw = P + wl;
           uint64_t a1 = min((hw + 1) & ~1ull, pw & ~1ull);
@@ -787,6 +878,9 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_pipe(PipeArgs a) {
           C.ring_off[s] = pos;
           head += need;
           C.ring_end[s] = head;
+          C.ring_head = head;
+          __threadfence_block();
+          C.lb_seq = i + 1;
           for (uint64_t w = a1; w < hw; ++w) dst[w - a0] = ldg_nc_u64(pay_g + w);
           const uint32_t bytes = (uint32_t)(8 * (a1 - a0));
           mbar_arrive_tx(&C.full_in[s], bytes);
@@ -794,24 +888,32 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_pipe(PipeArgs a) {
         } else {
           C.ring_off[s] = 0;
           C.ring_end[s] = head;
+          __threadfence_block();
+          C.lb_seq = i + 1;
           mbar_arrive(&C.full_in[s]);
         }
       }
+      __syncwarp();
     }
     return;
   }
+  if (warp >= NCW) return;  // spare warps
 
   // ------------------------------------------------------------ consumers
-  const int ctid = tid;
+  // No CTA barrier: a warp's block offsets come from a warp scan plus its
+  // group offset (map 0) or from OFF[] (map 1); each warp (or block group)
+  // bulk-stores its own part of the decoded tile; the stage is released when
+  // all NCW warps have arrived.
   const uint32_t L = (uint32_t)sh.Le;
   uint32_t err = 0;
+  const bool bst = a.bulk && !(a.debug & 4);
   for (uint32_t s = 0, ph = 0, s2 = 0;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0), s2 ^= 1u) {
     mbar_wait(&C.full_in[s], ph);
     const uint64_t t = C.tkt[s];
     if (t == TILE_NONE) break;
     const uint8_t* st = smem + sh.o_in + (size_t)s * sh.in_stride;
     const uint4* H = reinterpret_cast<const uint4*>(st);
-    uint32_t* OFF = reinterpret_cast<uint32_t*>(smem + sh.o_in + (size_t)s * sh.in_stride + sh.o_off);
+    const uint32_t* OFF = reinterpret_cast<const uint32_t*>(st + sh.o_off);
     const uint64_t* PAY = reinterpret_cast<const uint64_t*>(ring + C.ring_off[s]) + (C.P[s] & 1);
     const uint32_t terr = C.err[s];
     const uint64_t rend = C.ring_end[s];
@@ -821,122 +923,142 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_pipe(PipeArgs a) {
     const uint32_t nblk = (uint32_t)min((uint64_t)sh.TB, sh.n_blocks - b0);
     const uint64_t v0 = b0 * sh.Le;
     const uint32_t nv = (uint32_t)(min(sh.n, v0 + (uint64_t)sh.TB * sh.Le) - v0);
-    const bool bst = a.bulk && !(a.debug & 4);  // TMA bulk store of the tile (else coalesced STG)
-    const bool nostore = (a.debug & 8) != 0;
-    if (bst && ctid == 0) bulk_wait_read<1>();  // staging buffer s2 is free again
-    // in-tile word offsets of the blocks (a7): CTA scan of the n_words fields
-    // (a tile with W > words_cap was rejected by the look-back warp)
-    {
-      const uint32_t* Hw = reinterpret_cast<const uint32_t*>(H) + 3;
-      uint32_t base = 0;
-      for (uint32_t b0s = 0; b0s < nblk; b0s += PC) {
-        const uint32_t b = b0s + ctid;
-        const uint32_t x = (b < nblk && terr == 0) ? Hw[4 * b] : 0u;
+    uint8_t* og = a.out + v0 * sh.vb;
+    if (terr) err |= terr;
+    // this warp's staging regions were last bulk-stored two tiles ago
+    if (bst && lane == 0) bulk_wait_read<1>();
+    __syncwarp();
+    if (MAP == 0) {
+      for (uint32_t q = 0; q < sh.bpt; ++q) {
+        const uint32_t g0 = q * PC + warp * 32;  // first block of this warp group
+        if (g0 >= nblk) break;
+        const uint32_t b = g0 + lane;
+        const bool valid = b < nblk;
+        const uint4 h = valid ? H[b] : make_uint4(0, 0, 0, 0);
         uint32_t tot;
-        const uint32_t ex = cons_scan(x, &tot, C.scan[(b0s / PC) & 1]);
-        if (b < nblk) OFF[b] = base + ex;
-        base += tot;
-      }
-    }
-    cons_bar();
-    if (terr == 0 && !(a.debug & 1)) {
-      if (MAP == 0) {
-        for (uint32_t q = 0; q < sh.bpt; ++q) {
-          const uint32_t b = q * PC + ctid;
-          if (b >= nblk) break;
-          const uint4 h = H[b];
+        const uint32_t ex = warp_excl_scan((valid && !terr) ? h.w : 0u, &tot);
+        if (valid && !terr && !(a.debug & 1)) {
           const uint32_t nb = min(L, nv - b * L);
           V* dst = ob + (size_t)b * L;
           const uint32_t k = (h.x == CODEC_BASIC && h.z != 0) ? k_of(bc, (uint64_t)h.z + 1) : 1u;
           const uint32_t e = check_block_hdr(h, nb, sh.width, k);
           err |= e;
-          if (e) continue;
-          if (h.x == CODEC_CONSTANT) {
-            for (uint32_t j = 0; j < nb; ++j) dst[j] = (V)h.y;
-          } else {
-            const DecConst c = dconst_of(bc, (uint64_t)h.z + 1);
-            const uint64_t* src = PAY + OFF[b];
-            if (dc_log2b(c) == 32) {  // B = 2^32 (u32 only) does not fit the 32-bit multiplier
-              for (uint32_t j = 0, first = 0; j < h.w; ++j, first += k)
-                err |= decode_pow2<V>(src[j], 32, min(k, nb - first), h.y, dst + first);
+          if (!e) {
+            if (h.x == CODEC_CONSTANT) {
+              for (uint32_t j = 0; j < nb; ++j) dst[j] = (V)h.y;
             } else {
-              err |= decode_block_lane<V>(src, h.w, nb, c, h.z + 1, h.y, dst);
-            }
-          }
-        }
-      } else {
-        const uint32_t G = sh.G, nseg = nblk * G;
-        for (uint32_t seg = warp; seg < nseg; seg += NCW) {
-          const uint32_t b = seg / G, part = seg % G;
-          const uint4 h = H[b];
-          const uint32_t nb = min(L, nv - b * L);
-          V* dst = ob + (size_t)b * L;
-          const uint32_t k = (h.x == CODEC_BASIC && h.z != 0) ? k_of(bc, (uint64_t)h.z + 1) : 1u;
-          const uint32_t e = check_block_hdr(h, nb, sh.width, k);
-          err |= e;
-          if (e) continue;
-          if (h.x == CODEC_CONSTANT) {
-            const uint32_t lo = min(nb, part * sh.Lp), hi = min(nb, lo + sh.Lp);
-            for (uint32_t j = lo + lane; j < hi; j += 32) dst[j] = (V)h.y;
-          } else {
-            const DecConst c = dconst_of(bc, (uint64_t)h.z + 1);
-            const uint64_t* src = PAY + OFF[b];
-            uint32_t done = 0;
-            if (sizeof(V) == 2 && ((L * 2) & 15) == 0) {
-              uint8_t* blk = reinterpret_cast<uint8_t*>(dst);
-              const uint32_t Bu = h.z + 1;
-              switch (k) {
-#define POLY_UK(KK)                                                                                     \
-  case KK:                                                                                              \
-    err |= unpack_block_k<KK>(src, nb, c, Bu, h.y, part * 32 + lane, 32 * G, blk, &done);               \
-    break;
-                POLY_FOR_EACH_K16(POLY_UK)
-#undef POLY_UK
-                default:
-                  break;
+              const DecConst c = dconst_of(bc, (uint64_t)h.z + 1);
+              const uint64_t* src = PAY + OFF[q * NCW + warp] + ex;
+              if (dc_log2b(c) == 32) {  // B = 2^32 (u32 only) does not fit the 32-bit multiplier
+                for (uint32_t j = 0, first = 0; j < h.w; ++j, first += k)
+                  err |= decode_pow2<V>(src[j], 32, min(k, nb - first), h.y, dst + first);
+              } else {
+                const uint64_t P = (nb == L && h.z + 1 <= CACHE_B) ? bc.P[h.z + 1] : 0ull;
+                err |= decode_block_lane<V>(src, h.w, nb, c, h.z + 1, h.y, P, dst);
               }
             }
-            for (uint32_t j = done + part * 32 + lane; j < h.w; j += 32 * G) {
-              const uint32_t first = j * k;
-              err |= decode_any<V>(src[j], c, h.z, min(k, nb - first), h.y, dst + first);
+          }
+        }
+        // store the group's 32 blocks (bytes [g0 L vb, min(g0 + 32, nblk) L vb) clipped to nv)
+        const uint32_t lo = g0 * L * sh.vb, hi = min(nv, (g0 + 32) * L) * sh.vb;
+        if (bst) {
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0 && !(a.debug & 8)) {
+            const uint32_t b16 = (hi - lo) & ~15u;  // lo is 16-aligned: 32 L vb is a multiple of 64
+            if (b16) bulk_s2g(og + lo, ob8 + lo, b16);
+            for (uint32_t j = lo + b16; j < hi; ++j) og[j] = ob8[j];
+          }
+        } else {
+          __syncwarp();
+          for (uint32_t j = lo + lane; j < hi; j += 32) og[j] = ob8[j];
+        }
+      }
+    } else {
+      // map 1: part p of a block (G parts) decodes and stores one contiguous
+      // range of the block's values, so no warp waits for another
+      const uint32_t G = sh.G;
+      for (uint32_t seg = warp; seg < sh.TB * G; seg += NCW) {
+        const uint32_t b = seg / G, part = seg % G;
+        if (b >= nblk) break;
+        // the parts' ranges depend on k: every part's bulk store of two tiles
+        // ago has finished reading (waited above) before any part rewrites
+        if (G > 1) group_bar(2 + warp / G, 32 * G);
+        const uint4 h = H[b];
+        const uint32_t nb = min(L, nv - b * L);
+        V* dst = ob + (size_t)b * L;
+        uint32_t vlo = (uint32_t)(((uint64_t)nb * part / G) & ~7ull), vhi = part + 1 == G ? nb
+                                                                         : (uint32_t)(((uint64_t)nb * (part + 1) / G) & ~7ull);
+        if (!terr && !(a.debug & 1)) {
+          const uint32_t k = (h.x == CODEC_BASIC && h.z != 0) ? k_of(bc, (uint64_t)h.z + 1) : 1u;
+          const uint32_t e = check_block_hdr(h, nb, sh.width, k);
+          err |= e;
+          if (!e) {
+            if (h.x == CODEC_CONSTANT) {
+              for (uint32_t j = vlo + lane; j < vhi; j += 32) dst[j] = (V)h.y;
+            } else {
+              const DecConst c = dconst_of(bc, (uint64_t)h.z + 1);
+              const uint64_t* src = PAY + OFF[b];
+              bool spec = false;
+              if (sizeof(V) == 2 && ((L * 2) & 15) == 0) {
+                uint8_t* blk = reinterpret_cast<uint8_t*>(dst);
+                const uint32_t Bu = h.z + 1;
+                switch (k) {
+#define POLY_UK(KK)                                                                                       \
+  case KK: {                                                                                              \
+    const uint32_t ng = nb / kvals<KK>(), gb = ng * part / G, ge = ng * (part + 1) / G;                   \
+    err |= unpack_groups_k<KK>(src, gb, ge, c, Bu, h.y, blk);                                             \
+    vlo = gb * kvals<KK>();                                                                               \
+    vhi = part + 1 == G ? nb : ge * kvals<KK>();                                                          \
+    if (part + 1 == G)                                                                                    \
+      for (uint32_t j = ng * kq<KK>() + lane; j < h.w; j += 32)                                           \
+        err |= decode_any<V>(src[j], c, h.z, min(k, nb - j * k), h.y, dst + j * k);                       \
+    spec = true;                                                                                          \
+  } break;
+                  POLY_FOR_EACH_K16(POLY_UK)
+#undef POLY_UK
+                  default:
+                    break;
+                }
+              }
+              if (!spec) {  // generic: a contiguous range of words per part
+                const uint32_t jb = (uint32_t)((uint64_t)h.w * part / G), je = (uint32_t)((uint64_t)h.w * (part + 1) / G);
+                for (uint32_t j = jb + lane; j < je; j += 32)
+                  err |= decode_any<V>(src[j], c, h.z, min(k, nb - j * k), h.y, dst + j * k);
+                vlo = min(nb, jb * k);
+                vhi = min(nb, je * k);
+              }
             }
           }
         }
+        // store this part's range [vlo, vhi) of block b: bulk interior, plain edges
+        const uint32_t lo = (b * L + vlo) * sh.vb, hi = (b * L + vhi) * sh.vb;
+        if (bst) fence_proxy_async_smem();
+        __syncwarp();
+        const uint32_t a0 = min(hi, (lo + 15) & ~15u), a1 = max(a0, hi & ~15u);
+        if (bst && a1 > a0) {
+          if (lane == 0 && !(a.debug & 8)) bulk_s2g(og + a0, ob8 + a0, a1 - a0);
+          for (uint32_t j = lo + lane; j < a0; j += 32) og[j] = ob8[j];
+          for (uint32_t j = a1 + lane; j < hi; j += 32) og[j] = ob8[j];
+        } else {
+          for (uint32_t j = lo + lane; j < hi; j += 32) og[j] = ob8[j];
+        }
       }
-    } else if (ctid == 0) {
-      err |= terr;
     }
-    if (bst) fence_proxy_async_smem();
-    cons_bar();
-    uint8_t* og = a.out + v0 * sh.vb;
-    const uint32_t bytes = nv * sh.vb;
-    if (ctid == 0) {
-      __threadfence_block();
-      C.ring_tail = rend;  // the tile's payload words are consumed
+    __syncwarp();
+    if (lane == 0) {
+      if (bst) bulk_commit();  // one bulk group per warp and tile
+      // the last warp done with the stage frees its payload ring space (the
+      // stages complete in order: every warp finished the previous one)
+      if (atomicAdd(&C.done_cnt[s], 1u) == NCW - 1) {
+        C.done_cnt[s] = 0;
+        __threadfence_block();
+        C.ring_tail = rend;
+      }
       mbar_arrive(&C.empty_in[s]);
     }
-    if (nostore) {
-    } else if (bst) {
-      if (ctid == 0) {
-        const uint32_t b16 = bytes & ~15u;
-        if (b16) {
-          bulk_s2g(og, ob8, b16);
-          bulk_commit();
-        }
-        for (uint32_t j = b16; j < bytes; ++j) og[j] = ob8[j];
-      }
-    } else {
-      uint32_t done = 0;
-      if ((reinterpret_cast<uintptr_t>(og) & 15) == 0) {
-        const uint32_t n16 = bytes >> 4;
-        for (uint32_t j = ctid; j < n16; j += PC)
-          reinterpret_cast<uint4*>(og)[j] = reinterpret_cast<const uint4*>(ob8)[j];
-        done = n16 << 4;
-      }
-      for (uint32_t j = done + ctid; j < bytes; j += PC) og[j] = ob8[j];
-    }
   }
-  if (a.bulk && !(a.debug & 4) && ctid == 0) bulk_wait_all<0>();
+  if (bst && lane == 0) bulk_wait_all<0>();
   err = __reduce_or_sync(0xffffffffu, err);
   if (lane == 0 && err) atomicOr(a.status_out, err);
 }

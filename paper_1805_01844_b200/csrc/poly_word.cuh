@@ -14,6 +14,27 @@ __device__ __forceinline__ uint32_t ceil_div_small(uint32_t n, uint32_t k) {
   return q;
 }
 
+// One 64-bit fraction step (d, f) = (floor(f B / 2^64), f B mod 2^64), and
+// one 32-bit step (d, g) = (floor(g B / 2^32), g B mod 2^32).
+__device__ __forceinline__ uint32_t frac_step64(uint32_t& f0, uint32_t& f1, uint32_t B) {
+  uint32_t n0, n1, c, d;
+  asm("mul.lo.u32 %0, %4, %6;\n\t"
+      "mul.hi.u32 %1, %4, %6;\n\t"
+      "mad.lo.cc.u32 %2, %5, %6, %1;\n\t"
+      "madc.hi.u32 %3, %5, %6, 0;"
+      : "=&r"(n0), "=&r"(c), "=&r"(n1), "=r"(d)  // early clobber: outputs are written before the inputs are all read
+      : "r"(f0), "r"(f1), "r"(B));
+  f0 = n0;
+  f1 = n1;
+  return d;
+}
+__device__ __forceinline__ uint32_t frac_step32(uint32_t& g, uint32_t B) {
+  uint32_t lo, hi;
+  asm("mul.lo.u32 %0, %2, %3;\n\tmul.hi.u32 %1, %2, %3;" : "=&r"(lo), "=r"(hi) : "r"(g), "r"(B));
+  g = lo;
+  return hi;
+}
+
 // min / max of n values at s (one thread).  u16 at a 4-byte boundary: packed
 // u16x2 min/max over 32-bit words, four words per step.
 template <typename V>
@@ -265,104 +286,44 @@ __device__ __forceinline__ void pack_block_lane16(const uint16_t* v, uint32_t nb
   }
 }
 
-// Digits of two words in lock step (two independent chains), each word with
-// k digits of which the low m are written (out[i] = vmin + digit); digits at
-// i >= m must be 0.  Binary-fraction extraction as decode_frac.  Returns
-// POLY_ST_RESIDUE on a nonzero residue.
+// The top word of a full-length block: m < k digits, digits m..k-1 zero.
+// With P = B^(k-m), s' = s P < B^k iff s < B^m, and the digits of s are the
+// top m digits of s' -- so only m fraction steps are needed instead of k.
 template <typename V>
-__device__ __forceinline__ uint32_t decode_pair(uint64_t sa, uint64_t sb, const DecConst& c, uint32_t B,
-                                                uint32_t ma, uint32_t mb, uint32_t vmin, V* oa, V* ob) {
-  uint32_t extra = 0;
-  if (sa > c.Wmax || sb > c.Wmax) return POLY_ST_RESIDUE;
+__device__ __forceinline__ uint32_t decode_top_word(uint64_t s, const DecConst& c, uint32_t B, uint32_t m,
+                                                    uint64_t P, uint32_t vmin, V* out) {
+  const uint64_t sp = s * P;
+  if (__umul64hi(s, P) != 0 || sp > c.Wmax) return POLY_ST_RESIDUE;
   const uint32_t add = dc_add(c);
-  uint64_t fa, fb;
-  {
-    const uint64_t hi1 = __umul64hi(sa, c.Rl), lo2 = sa * c.Rh, hi2 = __umul64hi(sa, c.Rh), mid = lo2 + hi1;
-    fa = ((hi2 + (mid < lo2 ? 1ull : 0ull)) << 32) + (mid >> 32) + add;
-  }
-  {
-    const uint64_t hi1 = __umul64hi(sb, c.Rl), lo2 = sb * c.Rh, hi2 = __umul64hi(sb, c.Rh), mid = lo2 + hi1;
-    fb = ((hi2 + (mid < lo2 ? 1ull : 0ull)) << 32) + (mid >> 32) + add;
-  }
-  uint32_t a0 = (uint32_t)fa, a1 = (uint32_t)(fa >> 32), b0 = (uint32_t)fb, b1 = (uint32_t)(fb >> 32);
-  const int k = (int)dc_k(c), t = (int)dc_t32(c);
+  const uint64_t hi1 = __umul64hi(sp, c.Rl), lo2 = sp * c.Rh, hi2 = __umul64hi(sp, c.Rh), mid = lo2 + hi1;
+  const uint64_t f = ((hi2 + (mid < lo2 ? 1ull : 0ull)) << 32) + (mid >> 32) + add;
+  uint32_t f0 = (uint32_t)f, f1 = (uint32_t)(f >> 32);
+  const int k = (int)dc_k(c), t = (int)dc_t32(c), lo = k - (int)m;  // digits k-1 .. lo are the output
   int i = k - 1;
-  for (; i >= t; --i) {
-    const uint64_t ta = (uint64_t)a0 * B, tb = (uint64_t)b0 * B;
-    const uint64_t ua = (uint64_t)a1 * B + (uint32_t)(ta >> 32), ub = (uint64_t)b1 * B + (uint32_t)(tb >> 32);
-    const uint32_t da = (uint32_t)(ua >> 32), db = (uint32_t)(ub >> 32);
-    a1 = (uint32_t)ua;
-    a0 = (uint32_t)ta;
-    b1 = (uint32_t)ub;
-    b0 = (uint32_t)tb;
-    if ((uint32_t)i < ma) oa[i] = (V)(vmin + da); else extra |= da;
-    if ((uint32_t)i < mb) ob[i] = (V)(vmin + db); else extra |= db;
-  }
-  uint32_t ga = a1 + add, gb = b1 + add;
-  for (; i >= 0; --i) {
-    const uint64_t pa = (uint64_t)ga * B, pb = (uint64_t)gb * B;
-    const uint32_t da = (uint32_t)(pa >> 32), db = (uint32_t)(pb >> 32);
-    ga = (uint32_t)pa;
-    gb = (uint32_t)pb;
-    if ((uint32_t)i < ma) oa[i] = (V)(vmin + da); else extra |= da;
-    if ((uint32_t)i < mb) ob[i] = (V)(vmin + db); else extra |= db;
-  }
-  return extra ? POLY_ST_RESIDUE : 0u;
-}
-
-// Three words in lock step (three independent chains); see decode_pair.
-template <typename V>
-__device__ __forceinline__ uint32_t decode_triple(uint64_t sa, uint64_t sb, uint64_t sc, const DecConst& c,
-                                                  uint32_t B, uint32_t ma, uint32_t mb, uint32_t mc, uint32_t vmin,
-                                                  V* oa, V* ob, V* oc) {
-  uint32_t extra = 0;
-  if (sa > c.Wmax || sb > c.Wmax || sc > c.Wmax) return POLY_ST_RESIDUE;
-  const uint32_t add = dc_add(c);
-  uint64_t f[3];
-  const uint64_t sv[3] = {sa, sb, sc};
-#pragma unroll
-  for (int q = 0; q < 3; ++q) {
-    const uint64_t hi1 = __umul64hi(sv[q], c.Rl), lo2 = sv[q] * c.Rh, hi2 = __umul64hi(sv[q], c.Rh);
-    const uint64_t mid = lo2 + hi1;
-    f[q] = ((hi2 + (mid < lo2 ? 1ull : 0ull)) << 32) + (mid >> 32) + add;
-  }
-  uint32_t a0 = (uint32_t)f[0], a1 = (uint32_t)(f[0] >> 32), b0 = (uint32_t)f[1], b1 = (uint32_t)(f[1] >> 32);
-  uint32_t c0 = (uint32_t)f[2], c1 = (uint32_t)(f[2] >> 32);
-  const int k = (int)dc_k(c), t = (int)dc_t32(c);
-  int i = k - 1;
-  for (; i >= t; --i) {
-    const uint64_t ta = (uint64_t)a0 * B, tb = (uint64_t)b0 * B, tc = (uint64_t)c0 * B;
-    const uint64_t ua = (uint64_t)a1 * B + (uint32_t)(ta >> 32), ub = (uint64_t)b1 * B + (uint32_t)(tb >> 32);
-    const uint64_t uc = (uint64_t)c1 * B + (uint32_t)(tc >> 32);
-    const uint32_t da = (uint32_t)(ua >> 32), db = (uint32_t)(ub >> 32), dd = (uint32_t)(uc >> 32);
-    a1 = (uint32_t)ua; a0 = (uint32_t)ta;
-    b1 = (uint32_t)ub; b0 = (uint32_t)tb;
-    c1 = (uint32_t)uc; c0 = (uint32_t)tc;
-    if ((uint32_t)i < ma) oa[i] = (V)(vmin + da); else extra |= da;
-    if ((uint32_t)i < mb) ob[i] = (V)(vmin + db); else extra |= db;
-    if ((uint32_t)i < mc) oc[i] = (V)(vmin + dd); else extra |= dd;
-  }
-  uint32_t ga = a1 + add, gb = b1 + add, gc = c1 + add;
-  for (; i >= 0; --i) {
-    const uint64_t pa = (uint64_t)ga * B, pb = (uint64_t)gb * B, pc = (uint64_t)gc * B;
-    const uint32_t da = (uint32_t)(pa >> 32), db = (uint32_t)(pb >> 32), dd = (uint32_t)(pc >> 32);
-    ga = (uint32_t)pa; gb = (uint32_t)pb; gc = (uint32_t)pc;
-    if ((uint32_t)i < ma) oa[i] = (V)(vmin + da); else extra |= da;
-    if ((uint32_t)i < mb) ob[i] = (V)(vmin + db); else extra |= db;
-    if ((uint32_t)i < mc) oc[i] = (V)(vmin + dd); else extra |= dd;
-  }
-  return extra ? POLY_ST_RESIDUE : 0u;
+  V* o = out + (m - 1);
+#pragma unroll 1
+  for (; i >= max(t, lo); --i, --o) *o = (V)(vmin + frac_step64(f0, f1, B));
+  uint32_t g = f1 + add;
+#pragma unroll 1
+  for (; i >= lo; --i, --o) *o = (V)(vmin + frac_step32(g, B));
+  return 0u;
 }
 
 // All words of one block, one thread (B < 2^32).
+// P = B^(k - m_top) for the block's top word, or 0 (then the top word steps
+// through its zero digits).
 template <typename V>
 __device__ __forceinline__ uint32_t decode_block_lane(const uint64_t* src, uint32_t nw, uint32_t nb,
-                                                      const DecConst& c, uint32_t B, uint32_t vmin, V* out) {
+                                                      const DecConst& c, uint32_t B, uint32_t vmin, uint64_t P,
+                                                      V* out) {
   const uint32_t k = dc_k(c);
   uint32_t err = 0;
+  const uint32_t mt = nb - (nw - 1) * k;  // digits of the top word
+  const uint32_t nfast = (P != 0 && mt < k) ? nw - 1 : nw;
 #pragma unroll 1
-  for (uint32_t j = 0, first = 0; j < nw; ++j, first += k)
+  for (uint32_t j = 0, first = 0; j < nfast; ++j, first += k)
     err |= decode_frac<V>(src[j], c, B, min(k, nb - first), vmin, out + first);
+  if (nfast < nw) err |= decode_top_word<V>(src[nw - 1], c, B, mt, P, vmin, out + (nw - 1) * k);
   return err;
 }
 
@@ -373,27 +334,6 @@ __device__ __forceinline__ uint32_t decode_block_lane(const uint64_t* src, uint3
 //   64-bit step: (d, f) = (floor(f B / 2^64), f B mod 2^64);
 //   after k - t32 digits the top 32 bits + 1 are an exact 32-bit fraction for
 //   the last t32 digits: (d, g) = (floor(g B / 2^32), g B mod 2^32).
-// One 64-bit fraction step (d, f) = (floor(f B / 2^64), f B mod 2^64), and
-// one 32-bit step (d, g) = (floor(g B / 2^32), g B mod 2^32).
-__device__ __forceinline__ uint32_t frac_step64(uint32_t& f0, uint32_t& f1, uint32_t B) {
-  uint32_t n0, n1, c, d;
-  asm("mul.lo.u32 %0, %4, %6;\n\t"
-      "mul.hi.u32 %1, %4, %6;\n\t"
-      "mad.lo.cc.u32 %2, %5, %6, %1;\n\t"
-      "madc.hi.u32 %3, %5, %6, 0;"
-      : "=&r"(n0), "=&r"(c), "=&r"(n1), "=r"(d)  // early clobber: outputs are written before the inputs are all read
-      : "r"(f0), "r"(f1), "r"(B));
-  f0 = n0;
-  f1 = n1;
-  return d;
-}
-__device__ __forceinline__ uint32_t frac_step32(uint32_t& g, uint32_t B) {
-  uint32_t lo, hi;
-  asm("mul.lo.u32 %0, %2, %3;\n\tmul.hi.u32 %1, %2, %3;" : "=&r"(lo), "=r"(hi) : "r"(g), "r"(B));
-  g = lo;
-  return hi;
-}
-
 // Word -> its m low digits (out[i] = vmin + digit i, i < m), most significant
 // first; digits m..k-1 must be 0.  Plain loops (two digits per iteration): the
 // loop trip counts are the only thing that differs between lanes.

@@ -14,7 +14,7 @@ from typing import Optional, Tuple
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpolycomp.so")
+LIB_PATH = os.environ.get("POLY_LIB") or os.path.join(_HERE, "libpolycomp.so")  # POLY_LIB: A/B variants
 
 POLY_U16 = 16
 POLY_U32 = 32

@@ -127,8 +127,43 @@ def test_large_bases_u32(oracle_lib):
     check_case(oracle_lib, x, 0)
 
 
+# ------------------------------------------------------------------ large blocks
+# Blocks > 32 KiB with >= 256 blocks take the two-sweep large-block pipeline
+# (poly_large.cuh); ragged tails and every base class are covered.
+def _large_case(rng, w, L, nblocks, tail):
+    hi = 1 << w
+    blocks = []
+    for i in range(nblocks):
+        kind = i % 6
+        n = L if i < nblocks - 1 or tail == 0 else tail
+        if kind == 0:      # log-uniform base
+            b = int(2 ** rng.uniform(1, w)) if w == 16 else int(2 ** rng.uniform(1, 32))
+            b = max(2, min(b, hi))
+            v = rng.integers(0, b, size=n, dtype=np.uint64)
+        elif kind == 1:    # constant
+            v = np.full(n, int(rng.integers(0, hi)), dtype=np.uint64)
+        elif kind == 2:    # power-of-two base at the top of the range
+            j = int(rng.integers(1, w + 1))
+            v = rng.integers(0, 1 << j, size=n, dtype=np.uint64) + (hi - (1 << j))
+        elif kind == 3:    # full range
+            v = rng.integers(0, hi, size=n, dtype=np.uint64)
+        elif kind == 4:    # narrow noise
+            v = rng.integers(1000, 1013, size=n, dtype=np.uint64)
+        else:              # two values far apart
+            v = np.where(rng.random(n) < 0.5, 7, hi - 3).astype(np.uint64)
+        blocks.append(v)
+    return np.concatenate(blocks).astype(np.uint16 if w == 16 else np.uint32)
+
+
+@pytest.mark.parametrize("w,L,nblocks,tail", [(16, 20000, 260, 1234), (32, 10000, 258, 77), (16, 40000, 256, 0)])
+def test_large_blocks(oracle_lib, w, L, nblocks, tail):
+    rng = np.random.default_rng(w * 1000 + nblocks)
+    x = _large_case(rng, w, L, nblocks, tail)
+    check_case(oracle_lib, x, L)
+
+
 # ------------------------------------------------------------------ configs
-SMALL = {1: 1.0, 2: 1 / 100, 3: 1 / 64, 4: 1 / 128, 5: 1 / 128}
+SMALL = {1: 1.0, 2: 1 / 100, 3: 1 / 16, 4: 1 / 128, 5: 1 / 128}  # cfg3 at 1/16: 256 blocks (large-block pipeline)
 
 
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
