@@ -55,7 +55,7 @@ struct __align__(16) LargeCtl {
   uint64_t statsready[2], prefixready[2];
   // per stage
   uint64_t sb[MAXS];          // block of the stage (TILE_NONE = end)
-  uint32_t spass[MAXS], ssub[MAXS], snv[MAXS];
+  uint32_t spass[MAXS], ssub[MAXS], snv[MAXS], slast[MAXS];
   uint64_t sj0[MAXS], sj1[MAXS], sP[MAXS];  // decompress: words of the stage, block payload offset
   uint32_t serr[MAXS];
   uint4 shdr[MAXS];           // decompress: block header
@@ -138,6 +138,7 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_large(LargeArgs a) {
               C.spass[s] = pass;
               C.ssub[s] = c;
               C.snv[s] = nv;
+              C.slast[s] = c + 1 == nsub;
               const uint32_t b16 = bytes & ~15u;
               for (uint32_t j = b16; j < bytes; ++j) dst[j] = src[j];
               mbar_arrive_tx(&C.full_in[s], b16);
@@ -151,6 +152,7 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_large(LargeArgs a) {
               C.spass[s] = pass;
               C.ssub[s] = c;
               C.snv[s] = nv;
+              C.slast[s] = c + 1 == nsub;
               mbar_arrive(&C.full_in[s]);
             }
           }
@@ -203,10 +205,9 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_large(LargeArgs a) {
       }
       break;
     }
-    const uint32_t pass = C.spass[s], c = C.ssub[s], nv = C.snv[s];
+    const uint32_t pass = C.spass[s], c = C.ssub[s], nv = C.snv[s], last = C.slast[s];
     const V* sv = reinterpret_cast<const V*>(smem + sh.o_in + (size_t)s * sh.stage);
-    const uint64_t nb = blk_len(sh, b);
-    const uint32_t nsub = (uint32_t)((nb + sh.SV - 1) / sh.SV);
+    const uint32_t nb = (uint32_t)blk_len(sh, b);  // < 2^24 (block <= 4 MiB)
     if (pass == 0) {
       const uint32_t bs = iblk & 1u;
       // ---- a2: min / max of the sub-tile, warp slices, folded into the block's
@@ -217,14 +218,14 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_large(LargeArgs a) {
       if (lane == 0) {
         atomicMin(&C.bmin[bs], mn);
         atomicMax(&C.bmax[bs], mx);
-        if (c + 1 == nsub) {
+        if (last) {
           __threadfence_block();
           if (atomicAdd(&C.bcnt[bs], 1u) == NCW - 1) {  // the block's last contribution
             __threadfence_block();
             const uint32_t vmin = C.bmin[bs], vmax = C.bmax[bs];
             const uint64_t B = (uint64_t)vmax - vmin + 1;
             const uint32_t k = B == 1 ? 1u : capacity_of(B);
-            const uint64_t nw = B == 1 ? 0ull : (nb + k - 1) / k;
+            const uint64_t nw = B == 1 ? 0ull : ceil_div_small(nb, k);
             hdr_g[b] = make_uint4(B == 1 ? CODEC_CONSTANT : CODEC_BASIC, vmin, vmax - vmin, (uint32_t)nw);
             C.blk[bs] = b;
             C.bvmin[bs] = vmin;
@@ -239,7 +240,7 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_large(LargeArgs a) {
           }
         }
       }
-      if (c + 1 == nsub) ++iblk;
+      if (last) ++iblk;
     } else {
       // ---- a5: words whose first value lies in this sub-tile, straight to HBM
       const uint32_t bs = (iblk - 1) & 1u;  // the block of sweep 1 is the last one started
@@ -248,13 +249,30 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_large(LargeArgs a) {
       if (bm1 != 0) {
         const uint32_t vmin = C.bvmin[bs], k = C.bk[bs];
         const uint64_t B = (uint64_t)bm1 + 1;
-        const uint64_t v0 = (uint64_t)c * sh.SV;
-        const uint64_t jb = (v0 + k - 1) / k;
-        const uint64_t je = min((uint64_t)C.bnw[bs], (v0 + nv + k - 1) / k);
+        const uint32_t v0 = c * sh.SV;
+        const uint32_t jb = ceil_div_small(v0, k);
+        const uint32_t je = min(C.bnw[bs], ceil_div_small(v0 + nv, k));
         uint64_t* dst = pay_g + C.bP[bs];
-        for (uint64_t j = jb + (uint32_t)(warp * 32 + lane); j < je; j += PC) {
-          const uint64_t first = j * k;
-          dst[j] = pack_word64<V>(sv + (first - v0), (uint32_t)min((uint64_t)k, nb - first), B, vmin);
+        // two words per thread per step: two independent Horner chains
+        for (uint32_t j = jb + (uint32_t)(warp * 32 + lane); j < je; j += 2 * PC) {
+          const uint32_t j2 = j + PC, f1 = j * k, f2 = j2 * k;
+          const uint32_t m1 = min(k, nb - f1);
+          if (j2 < je && m1 == k && f2 + k <= nb && B < (1ull << 32)) {
+            const V* p1 = sv + (f1 - v0);
+            const V* p2 = sv + (f2 - v0);
+            const uint32_t Bu = (uint32_t)B;
+            uint64_t s1 = 0, s2 = 0;
+#pragma unroll 4
+            for (int i = (int)k - 1; i >= 0; --i) {
+              s1 = s1 * Bu + ((uint32_t)p1[i] - vmin);
+              s2 = s2 * Bu + ((uint32_t)p2[i] - vmin);
+            }
+            dst[j] = s1;
+            dst[j2] = s2;
+          } else {
+            dst[j] = pack_word64<V>(sv + (f1 - v0), m1, B, vmin);
+            if (j2 < je) dst[j2] = pack_word64<V>(sv + (f2 - v0), min(k, nb - f2), B, vmin);
+          }
         }
       }
     }
@@ -416,17 +434,18 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_large(LargeArgs a) {
       } else {
         const DecConst dc = C.sdc[s];
         const uint32_t k = dc_k(dc);
-        for (uint64_t j = j0 + tid; j < j1; j += PC) {
-          const uint64_t first = j * k;
-          const uint32_t m = (uint32_t)min((uint64_t)k, nb - first);
-          if (first >= v0 && first + m <= v0 + nv) {  // the word lies inside the sub-tile
-            err |= decode_any<V>(words[j - j0], dc, h.z, m, h.y, ob + (first - v0));
+        const uint32_t nb32 = (uint32_t)nb, v032 = (uint32_t)v0, jn = (uint32_t)(j1 - j0), j032 = (uint32_t)j0;
+        for (uint32_t jj = tid; jj < jn; jj += PC) {
+          const uint32_t first = (j032 + jj) * k;  // < 2^24: block <= 4 MiB
+          const uint32_t m = min(k, nb32 - first);
+          if (first >= v032 && first + m <= v032 + nv) {  // the word lies inside the sub-tile
+            err |= decode_any<V>(words[jj], dc, h.z, m, h.y, ob + (first - v032));
           } else {  // crosses a sub-tile edge: decode to scratch, keep the part inside
             V tmp[64];
-            err |= decode_any<V>(words[j - j0], dc, h.z, m, h.y, tmp);
+            err |= decode_any<V>(words[jj], dc, h.z, m, h.y, tmp);
             for (uint32_t i = 0; i < m; ++i) {
-              const uint64_t p = first + i;
-              if (p >= v0 && p < v0 + nv) ob[p - v0] = tmp[i];
+              const uint32_t p = first + i;
+              if (p >= v032 && p < v032 + nv) ob[p - v032] = tmp[i];
             }
           }
         }
