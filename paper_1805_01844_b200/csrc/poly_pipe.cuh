@@ -110,7 +110,6 @@ struct __align__(16) PipeCtl {
   uint64_t rec_t[MAXR], rec_W[MAXR], rec_end[MAXR];  // compress: staged tiles
   uint64_t rec_empty[MAXR];
   uint32_t rec_off[MAXR];
-  uint32_t cur_off;         // compress: ring offset of the tile being packed
   volatile uint32_t wdone;  // compress: records completed, in order
   uint32_t scan[2][NCW];
   uint64_t payload_words;
@@ -390,7 +389,7 @@ __device__ __forceinline__ void warp_copy(uint8_t* dst, const uint8_t* src, uint
 // compress
 // ======================================================================
 template <typename V, int MAP>
-__global__ void __launch_bounds__(PT, 1) poly_compress_pipe(PipeArgs a) {
+__global__ void __launch_bounds__(PT, POLY_CTAS) poly_compress_pipe(PipeArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   PipeCtl& C = *reinterpret_cast<PipeCtl*>(smem);
   const PipeShape& sh = a.sh;
@@ -401,10 +400,10 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_pipe(PipeArgs a) {
   if (tid == 0) {
     for (uint32_t s = 0; s < S; ++s) {
       mbar_init(&C.full_in[s], 1);
-      mbar_init(&C.empty_in[s], 1);
+      mbar_init(&C.empty_in[s], NCW);
     }
     for (int r = 0; r < MAXR; ++r) {
-      mbar_init(&C.rec_full[r], 1);
+      mbar_init(&C.rec_full[r], NCW);
       mbar_init(&C.rec_empty[r], 1);
     }
     C.ring_tail = 0;
@@ -511,11 +510,11 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_pipe(PipeArgs a) {
        s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0), r = (r + 1) % MAXR, rph ^= (r == 0)) {
     mbar_wait(&C.full_in[s], ph);
     const uint64_t t = C.tkt[s];
-    if (t == TILE_NONE) {  // one end marker per writer warp
-      if (ctid == 0) {
+    if (t == TILE_NONE) {  // one end marker per writer warp (every consumer warp arrives)
+      if (lane == 0) {
         for (int e = 0; e < NWRITERS; ++e) {
           mbar_wait(&C.rec_empty[r], rph ^ 1u);
-          C.rec_t[r] = TILE_NONE;
+          if (warp == 0) C.rec_t[r] = TILE_NONE;
           mbar_arrive(&C.rec_full[r]);
           r = (r + 1) % MAXR;
           rph ^= (r == 0);
@@ -614,14 +613,13 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_pipe(PipeArgs a) {
       }
       __threadfence_block();
       head += need;
-      C.cur_off = pos;
       C.rec_t[r] = t;
       C.rec_W[r] = W;
       C.rec_off[r] = pos;
       C.rec_end[r] = head;
     }
     cons_bar();
-    uint64_t* ow = reinterpret_cast<uint64_t*>(ring + C.cur_off);
+    uint64_t* ow = reinterpret_cast<uint64_t*>(ring + C.rec_off[r]);
 
     // ---- a5: Horner pack
     if (MAP == 0) {
@@ -673,8 +671,10 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_pipe(PipeArgs a) {
         }
       }
     }
-    cons_bar();
-    if (ctid == 0) {
+    // every warp reports its own end: the record is complete and the input
+    // stage free once all NCW warps have arrived (no CTA barrier)
+    __syncwarp();
+    if (lane == 0) {
       mbar_arrive(&C.rec_full[r]);
       mbar_arrive(&C.empty_in[s]);
     }
@@ -702,6 +702,26 @@ __device__ __forceinline__ uint32_t check_global_header_p(const PipeArgs& a, uin
   return 0;
 }
 
+// The words of a block past its full k-specialised groups (at most Q full
+// words and the top word), one lane each; the top word of a full-length block
+// takes the premultiplied path (m steps, not k).
+template <typename V>
+__device__ __forceinline__ uint32_t decode_tail(const uint64_t* src, uint32_t j0, uint32_t nw, const DecConst& c,
+                                                uint32_t B, uint32_t vmin, uint32_t nb, uint32_t k, V* dst,
+                                                const BaseCache& bc, uint32_t L) {
+  uint32_t err = 0;
+  const uint32_t j = j0 + (threadIdx.x & 31);
+  if (j < nw) {
+    const uint32_t first = j * k, m = min(k, nb - first);
+    const uint64_t P = (m < k && nb == L && B <= CACHE_B) ? bc.P[B] : 0ull;
+    if (P != 0 && dc_log2b(c) != 32)
+      err = decode_top_word<V>(src[j], c, B, m, P, vmin, dst + first);
+    else
+      err = decode_any<V>(src[j], c, B - 1, m, vmin, dst + first);
+  }
+  return err;
+}
+
 template <typename V, int MAP>
 __global__ void __launch_bounds__(PT, POLY_CTAS) poly_decompress_pipe(PipeArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -727,7 +747,7 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_decompress_pipe(PipeArgs a
     C.lb_seq = 0;
     C.ring_head = 0;
   }
-  cache_fill(bc, true, MAP == 0 ? sh.Le : 0);
+  cache_fill(bc, true, sh.Le);
   __syncthreads();
   if (C.hdr_err) {  // same verdict in every CTA: nothing is decoded, no look-back
     if (blockIdx.x == 0 && tid == 0) atomicOr(a.status_out, C.hdr_err);
@@ -1011,8 +1031,7 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_decompress_pipe(PipeArgs a
     vlo = gb * kvals<KK>();                                                                               \
     vhi = part + 1 == G ? nb : ge * kvals<KK>();                                                          \
     if (part + 1 == G)                                                                                    \
-      for (uint32_t j = ng * kq<KK>() + lane; j < h.w; j += 32)                                           \
-        err |= decode_any<V>(src[j], c, h.z, min(k, nb - j * k), h.y, dst + j * k);                       \
+      err |= decode_tail(src, ng * kq<KK>(), h.w, c, Bu, h.y, nb, k, dst, bc, L);                          \
     spec = true;                                                                                          \
   } break;
                   POLY_FOR_EACH_K16(POLY_UK)
