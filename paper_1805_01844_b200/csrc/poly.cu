@@ -316,10 +316,10 @@ uint32_t debug_flags() {
   return e ? (uint32_t)strtoul(e, nullptr, 0) : 0u;
 }
 // Look-back warps per CTA (1 or 2); POLY_LB overrides the default.
-uint32_t lb_warps(uint32_t dflt) {
+uint32_t lb_warps(uint32_t dflt, uint32_t vmax) {
   const char* e = getenv("POLY_LB");
   const uint32_t v = e ? (uint32_t)strtoul(e, nullptr, 0) : dflt;
-  return v == 2 ? 2u : 1u;
+  return std::max(1u, std::min(v, vmax));
 }
 
 template <typename K>
@@ -329,6 +329,18 @@ int pipe_grid(K kernel, uint32_t smem, uint64_t tiles, int dev) {
     per_sm = 1;
   const uint64_t cap = (uint64_t)(g_sms[dev] > 0 ? g_sms[dev] : 148) * per_sm;
   return (int)std::max<uint64_t>(1, std::min<uint64_t>(cap, tiles));
+}
+// Grid of a pipeline launch: worker CTAs plus, when there is more than one
+// tile, the prefix-server CTA (all resident: the grid never exceeds what fits).
+// POLY_SERVER=0 selects the in-worker decoupled look-back instead.
+template <typename K>
+int pipe_grid_server(K kernel, uint32_t smem, uint64_t tiles, int dev, uint32_t& server) {
+  const char* e = getenv("POLY_SERVER");
+  const bool want = !(e && e[0] == '0');
+  const int cap = pipe_grid(kernel, smem, ~0ull, dev);
+  server = (want && tiles > 1 && cap >= 2) ? 1u : 0u;
+  const uint64_t workers = std::min<uint64_t>(tiles, (uint64_t)cap - server);
+  return (int)(std::max<uint64_t>(1, workers) + server);
 }
 
 }  // namespace
@@ -369,6 +381,20 @@ uint64_t poly_workspace_bytes(uint64_t n, poly_dtype_t dt, uint64_t block_size) 
   if (!plan(n, (uint32_t)dt, block_size, sh, rg)) return 0;
   return ws_layout(sh, rg).total;
 }
+
+#ifdef POLY_TRACE
+// Timing experiments only (not in include/poly.h): the pipeline event trace.
+int poly_trace_reset(void) {
+  void* p = nullptr;
+  if (cudaGetSymbolAddress(&p, polyk::g_trace) != cudaSuccess) return 1;
+  return cudaMemset(p, 0xff, sizeof(polyk::g_trace)) == cudaSuccess ? 0 : 1;
+}
+int poly_trace_dump(void* host, uint64_t bytes) {
+  if (bytes > sizeof(polyk::g_trace)) bytes = sizeof(polyk::g_trace);
+  return cudaMemcpyFromSymbol(host, polyk::g_trace, bytes) == cudaSuccess ? 0 : 1;
+}
+uint64_t poly_trace_bytes(void) { return sizeof(polyk::g_trace); }
+#endif
 
 int poly_launches_per_call(uint64_t n, poly_dtype_t dt, uint64_t block_size, int decompress) {
   Shape sh;
@@ -434,10 +460,11 @@ poly_status_t poly_compress(const void* d_in, uint64_t n, poly_dtype_t dt, uint6
     pa.ticket = a.ticket;
     pa.bulk = ((reinterpret_cast<uintptr_t>(d_in) & 15) == 0 && pa.sh.tile_bytes % 16 == 0) ? 1u : 0u;
     pa.debug = debug_flags();
-    pa.nlb = lb_warps(1);
+    pa.nlb = lb_warps(2, NLB_MAX + 1);
     auto k = dt == POLY_U16 ? (pa.sh.map == 0 ? poly_compress_pipe<uint16_t, 0> : poly_compress_pipe<uint16_t, 1>)
                             : (pa.sh.map == 0 ? poly_compress_pipe<uint32_t, 0> : poly_compress_pipe<uint32_t, 1>);
-    k<<<pipe_grid(k, pa.sh.smem, pa.sh.n_tiles, dev), PT, pa.sh.smem, s>>>(pa);
+    const int grid = pipe_grid_server(k, pa.sh.smem, pa.sh.n_tiles, dev, pa.server);
+    k<<<grid, PT, pa.sh.smem, s>>>(pa);
   } else {
     a.bmin = reinterpret_cast<uint32_t*>(ws + W.bmin_off);
     a.bmax = reinterpret_cast<uint32_t*>(ws + W.bmax_off);
@@ -538,11 +565,14 @@ poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_
     pa.ticket = a.ticket;
     pa.bulk = ((reinterpret_cast<uintptr_t>(d_out) & 15) == 0 && pa.sh.tile_bytes % 16 == 0) ? 1u : 0u;
     pa.debug = debug_flags();
-    pa.nlb = lb_warps(1);
+    // a look-back warp waits on stage i's barrier only after finishing stage
+    // i - nlb, so nlb <= S keeps every parity wait within one phase
+    pa.nlb = lb_warps(2, std::min<uint32_t>(NLB_MAX, pa.sh.S));
     auto k = dt == POLY_U16
                  ? (pa.sh.map == 0 ? poly_decompress_pipe<uint16_t, 0> : poly_decompress_pipe<uint16_t, 1>)
                  : (pa.sh.map == 0 ? poly_decompress_pipe<uint32_t, 0> : poly_decompress_pipe<uint32_t, 1>);
-    k<<<pipe_grid(k, pa.sh.smem, pa.sh.n_tiles, dev), PT, pa.sh.smem, s>>>(pa);
+    const int grid = pipe_grid_server(k, pa.sh.smem, pa.sh.n_tiles, dev, pa.server);
+    k<<<grid, PT, pa.sh.smem, s>>>(pa);
   } else {
     a.woff = reinterpret_cast<uint64_t*>(ws + W.woff_off);
     cudaMemsetAsync(ws, 0, W.bmin_off, s);

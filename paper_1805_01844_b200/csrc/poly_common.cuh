@@ -232,6 +232,17 @@ __device__ __forceinline__ uint64_t lookback_wide(const uint64_t* status, uint64
   uint64_t excl = 0;
   int64_t base = (int64_t)tile - 1;  // lane l covers base - LB_PER*l - j, j = 0..LB_PER-1
   uint32_t ns = 0;
+  // Cheap wait first: one lane polls the predecessor's status word until it
+  // is published (statuses appear roughly in tile order, so by then most of
+  // the window is valid); the wide reads below then rarely repeat.
+  if (lane == 0) {
+    uint32_t w = 0;
+    while (ld_relaxed_u64(status + base) == 0) {
+      if (w) __nanosleep(w);
+      w = w ? min(w * 2, 256u) : 32u;
+    }
+  }
+  __syncwarp();
   while (true) {
     uint64_t e[LB_PER];
     const int64_t top = base - (int64_t)LB_PER * lane;
@@ -260,7 +271,7 @@ __device__ __forceinline__ uint64_t lookback_wide(const uint64_t* status, uint64
     }
     if (binv) {
       if (ns) __nanosleep(ns);
-      ns = ns ? min(ns * 2, 128u) : 32u;
+      ns = ns ? min(ns * 2, 256u) : 32u;
       continue;
     }
     uint64_t sum = 0;

@@ -36,16 +36,38 @@ namespace polyk {
 #ifndef POLY_CTAS
 #define POLY_CTAS 1  // CTAs per SM the shared-memory plan targets
 #endif
+
+// POLY_TRACE (timing experiments only, a separate library variant): per CTA
+// and per tile (the CTA's i-th tile), globaltimer stamps of pipeline events,
+// read back with poly_trace_dump (profiles/trace_run.py).
+#ifdef POLY_TRACE
+constexpr uint32_t TRACE_TILES = 1024, TRACE_EV = 16;
+__device__ uint64_t g_trace[160 * TRACE_TILES * TRACE_EV];
+__device__ __forceinline__ void trace_ev(uint32_t i, int e, uint64_t v = ~0ull) {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (i < TRACE_TILES) g_trace[((size_t)blockIdx.x * TRACE_TILES + i) * TRACE_EV + e] = v == ~0ull ? t : v;
+}
+#define TRACE(i, e) trace_ev((i), (e))
+#define TRACE_V(i, e, v) trace_ev((i), (e), (v))
+#else
+#define TRACE(i, e)
+#define TRACE_V(i, e, v)
+#endif
 constexpr int NCW = POLY_NCW;      // consumer warps
 constexpr int PC = NCW * 32;       // consumer threads
-constexpr int PT = PC + 128;       // + producer, writer(s), header-sum and 2nd look-back warps
+#ifndef POLY_NLB_MAX
+#define POLY_NLB_MAX 4
+#endif
+constexpr int NLB_MAX = POLY_NLB_MAX;  // look-back warps per CTA (upper bound)
+constexpr int PT = PC + 32 * (2 + NLB_MAX);  // + producer, header-sum and look-back / writer warps
 constexpr int W_PROD = NCW;        // warp index of the producer / header issuer
-constexpr int W_WRIT = NCW + 1;    // warp index of the writer / look-back warp
-constexpr int W_HSUM = NCW + 2;    // decompress: header-sum warp (compress: 2nd writer)
-constexpr int W_LB2 = NCW + 3;     // decompress: 2nd look-back warp
-constexpr int NWRITERS = 1;        // compress writer warps
-// Look-back warps per CTA (compress writers / decompress look-back warps):
-// PipeArgs.nlb = 1 or 2 (host: POLY_LB env, default below).
+constexpr int W_WRIT = NCW + 1;    // first writer (compress) / look-back (decompress) warp
+constexpr int W_HSUM = NCW + 2;    // decompress: header-sum warp (compress: a writer)
+constexpr int W_LBX = NCW + 3;     // decompress: look-back warps 2 .. NLB_MAX
+// PipeArgs.nlb = look-back warps in use: compress writers W_WRIT .. W_WRIT +
+// nlb - 1 (nlb <= NLB_MAX + 1), decompress W_WRIT and W_LBX .. (nlb <= NLB_MAX)
+// (host: POLY_LB env, defaults in poly.cu).
 constexpr int MAXS = 8;            // max ring stages
 constexpr int BPT_MAX = 2;         // map 0: blocks per consumer thread
 constexpr uint32_t PIPE_MAX_BLOCK = 32768;  // bytes per block handled here
@@ -88,8 +110,8 @@ struct PipeArgs {
   uint32_t* ticket;
   uint32_t bulk;            // value array 16-byte aligned and tile_bytes % 16 == 0
   uint32_t debug;           // timing experiments only (POLY_DEBUG): 1 skip compute, 2 skip look-back
-  uint32_t nlb;             // look-back warps (1 or 2)
-  uint32_t pad2;
+  uint32_t nlb;             // look-back / writer warps in use
+  uint32_t server;          // 1: the last CTA is the prefix server (see prefix_server)
   PipeShape sh;
 };
 
@@ -230,12 +252,21 @@ __device__ __forceinline__ uint32_t cons_scan(uint32_t x, uint32_t* total, uint3
 // Shared-memory cache of the per-base table for B <= CACHE_B (SoA so that
 // lanes with nearby bases hit different banks).  cmeta = DecConst.meta
 // (k | log2b << 8 | t32 << 16 | h << 24).
+// Decoder constants of one base, with the L-dependent shape of a full block
+// (48 bytes: three 16-byte shared-memory loads).
+struct __align__(16) DecEnt {
+  uint64_t Rl, Rh;  // fraction reciprocal (DecConst)
+  uint64_t Wmax;    // B^k - 1
+  uint64_t P;       // B^(k - mt): premultiplier of an L-block's top word (1 if full)
+  uint32_t meta;    // as DecConst
+  uint32_t nwL;     // words of an L-block = ceil(L / k)
+  uint32_t mt;      // digits of an L-block's top word
+  uint32_t pad;
+};
+
 struct BaseCache {
-  uint64_t* P;   // decompress map 0: B^(k - m_top(L)), 0 if the top word of an L-block is full
-  uint32_t* meta;
-  uint64_t* Bk;  // decompress: Wmax = B^k - 1
-  uint64_t* Rl;  // decompress: ceil(2^160 / B^k), low / high 64 bits
-  uint64_t* Rh;
+  DecEnt* E;     // decompress
+  uint32_t* meta;  // compress
   uint64_t* D;   // compress: B^h
   uint32_t* G;   // compress: 1 + B + ... + B^(h-1) mod 2^32
 };
@@ -244,45 +275,44 @@ __device__ __forceinline__ BaseCache cache_at(uint8_t* base, bool dec) {
   BaseCache c;
   uint64_t* p = reinterpret_cast<uint64_t*>(base);
   if (dec) {
-    c.Bk = p;
-    c.Rl = p + (CACHE_B + 1);
-    c.Rh = p + 2 * (CACHE_B + 1);
-    c.P = p + 3 * (CACHE_B + 1);
-    c.meta = reinterpret_cast<uint32_t*>(p + 4 * (CACHE_B + 1));
+    c.E = reinterpret_cast<DecEnt*>(base);
+    c.meta = nullptr;
     c.D = nullptr;
     c.G = nullptr;
   } else {
-    c.P = nullptr;
+    c.E = nullptr;
     c.D = p;
     c.meta = reinterpret_cast<uint32_t*>(p + (CACHE_B + 1));
     c.G = c.meta + (CACHE_B + 1);
-    c.Bk = c.Rl = c.Rh = nullptr;
   }
   return c;
 }
 __host__ __device__ constexpr uint32_t cache_bytes(bool dec) {
-  return dec ? (uint32_t)(4 * 8 * (CACHE_B + 1) + 4 * (CACHE_B + 1) + 15) / 16 * 16
+  return dec ? (uint32_t)(sizeof(DecEnt) * (CACHE_B + 1) + 15) / 16 * 16
              : (uint32_t)(8 * (CACHE_B + 1) + 8 * (CACHE_B + 1) + 15) / 16 * 16;
 }
 __device__ __forceinline__ void cache_fill(const BaseCache& c, bool dec, uint64_t L = 0) {
   for (uint32_t B = threadIdx.x; B <= CACHE_B; B += blockDim.x) {
     const DecConst d = g_dtab[B];
-    c.meta[B] = d.meta;
     if (dec) {
-      c.Bk[B] = d.Wmax;
-      c.Rl[B] = d.Rl;
-      c.Rh[B] = d.Rh;
-      uint64_t P = 0;
+      DecEnt e;
+      e.Rl = d.Rl;
+      e.Rh = d.Rh;
+      e.Wmax = d.Wmax;
+      e.meta = d.meta;
+      e.P = 1;
+      e.nwL = 0;
+      e.mt = 0;
+      e.pad = 0;
       const uint32_t k = d.meta & 0xffu;
       if (B >= 2 && L != 0 && k != 0) {
-        const uint64_t mt = L - ((L + k - 1) / k - 1) * k;  // digits of an L-block's top word
-        if (mt < k) {
-          P = 1;
-          for (uint32_t i = 0; i < k - mt; ++i) P *= B;
-        }
+        e.nwL = (uint32_t)((L + k - 1) / k);
+        e.mt = (uint32_t)(L - (uint64_t)(e.nwL - 1) * k);  // 1 .. k
+        for (uint32_t i = e.mt; i < k; ++i) e.P *= B;
       }
-      c.P[B] = P;
+      c.E[B] = e;
     } else {
+      c.meta[B] = d.meta;
       const uint32_t h = d.meta >> 24;
       uint64_t D = 1;
       uint32_t G = 0;
@@ -309,9 +339,13 @@ __device__ __forceinline__ void chunk_consts(const BaseCache& c, uint32_t B, uin
     D *= B;
   }
 }
-// k (values per u64 word) for 2 <= B <= 2^32.
+// k (values per u64 word) for 2 <= B <= 2^32 (compress / decompress caches).
 __device__ __forceinline__ uint32_t k_of(const BaseCache& c, uint64_t B) {
   if (B <= CACHE_B) return c.meta[B] & 0xffu;
+  return capacity_of(B);
+}
+__device__ __forceinline__ uint32_t dk_of(const BaseCache& c, uint64_t B) {
+  if (B <= CACHE_B) return c.E[B].meta & 0xffu;
   return capacity_of(B);
 }
 // k and h (values per 32-bit chunk) for 2 <= B <= 2^16.
@@ -321,11 +355,12 @@ __device__ __forceinline__ uint32_t kh_of16(const BaseCache& c, uint32_t B) {
 }
 __device__ __forceinline__ DecConst dconst_of(const BaseCache& c, uint64_t B) {
   if (B <= CACHE_B) {
+    const DecEnt& e = c.E[B];
     DecConst d;
-    d.Wmax = c.Bk[B];
-    d.Rl = c.Rl[B];
-    d.Rh = c.Rh[B];
-    d.meta = c.meta[B];
+    d.Wmax = e.Wmax;
+    d.Rl = e.Rl;
+    d.Rh = e.Rh;
+    d.meta = e.meta;
     d.pad = 0;
     return d;
   }
@@ -386,11 +421,85 @@ __device__ __forceinline__ void warp_copy(uint8_t* dst, const uint8_t* src, uint
 }
 
 // ======================================================================
+// tile prefixes (a4)
+// ======================================================================
+// Prefix server: the last CTA of the grid runs no tiles; one warp turns the
+// tiles' published aggregates (FLAG_AGG | words) into inclusive prefixes
+// (FLAG_PRE | words up to and including the tile), in tile order, 256 tiles
+// per read.  Its SM carries no bulk traffic, so its reads return quickly; a
+// worker then needs one word, status[t - 1], to learn its tile's offset
+// instead of walking back through other tiles.
+__device__ __noinline__ void prefix_server(uint64_t* status, uint64_t n_tiles) {
+  const int lane = threadIdx.x & 31;
+  uint64_t P = 0, f = 0;
+  uint32_t ns = 0;
+  while (f < n_tiles) {
+    uint64_t e[LB_PER];
+    uint32_t lv = LB_PER;  // this lane's first unpublished slot
+#pragma unroll
+    for (int j = 0; j < LB_PER; ++j) {
+      const uint64_t idx = f + (uint64_t)(LB_PER * lane + j);
+      e[j] = idx < n_tiles ? ld_relaxed_u64(status + idx) : 0ull;
+    }
+#pragma unroll
+    for (int j = LB_PER - 1; j >= 0; --j)
+      if ((e[j] >> 62) == 0) lv = j;
+    const uint32_t bad = __ballot_sync(0xffffffffu, lv < LB_PER);
+    const int l0 = bad ? __ffs(bad) - 1 : 32;
+    const uint32_t q = l0 == 32 ? 32 * LB_PER : LB_PER * l0 + __shfl_sync(0xffffffffu, lv, l0 & 31);
+    if (q == 0) {
+      if (ns) __nanosleep(ns);
+      ns = ns ? min(ns * 2, 128u) : 32u;
+      continue;
+    }
+    ns = 0;
+    // inclusive prefixes of the run [f, f + q)
+    uint64_t loc[LB_PER], run = 0;
+#pragma unroll
+    for (int j = 0; j < LB_PER; ++j) {
+      if ((uint32_t)(LB_PER * lane + j) < q) run += e[j] & VAL_MASK;
+      loc[j] = run;
+    }
+    uint64_t inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const uint64_t excl = P + inc - run;
+#pragma unroll
+    for (int j = 0; j < LB_PER; ++j)
+      if ((uint32_t)(LB_PER * lane + j) < q)
+        st_relaxed_u64(status + f + LB_PER * lane + j, FLAG_PRE | ((excl + loc[j]) & VAL_MASK));
+    P += __shfl_sync(0xffffffffu, inc, 31);
+    f += q;
+  }
+}
+
+// A worker's exclusive prefix for tile t >= 1: the server's inclusive prefix
+// of tile t - 1 (one word, polled by lane 0).
+__device__ __forceinline__ uint64_t wait_prefix(const uint64_t* status, uint64_t t) {
+  uint64_t v = 0;
+  if ((threadIdx.x & 31) == 0) {
+    uint32_t ns = 0;
+    while (((v = ld_relaxed_u64(status + t - 1)) >> 62) != 2) {
+      if (ns) __nanosleep(ns);
+      ns = ns ? min(ns * 2, 256u) : 64u;
+    }
+  }
+  return __shfl_sync(0xffffffffu, v, 0) & VAL_MASK;
+}
+
+// ======================================================================
 // compress
 // ======================================================================
 template <typename V, int MAP>
 __global__ void __launch_bounds__(PT, POLY_CTAS) poly_compress_pipe(PipeArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
+  if (a.server && blockIdx.x == gridDim.x - 1) {
+    if (threadIdx.x < 32) prefix_server(a.status, a.sh.n_tiles);
+    return;
+  }
   PipeCtl& C = *reinterpret_cast<PipeCtl*>(smem);
   const PipeShape& sh = a.sh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -418,10 +527,14 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_compress_pipe(PipeArgs a) 
   if (warp == W_PROD) {
     // ---------------------------------------------------------- producer
     const uint64_t total_bytes = sh.n * sh.vb;
-    for (uint32_t s = 0, ph = 0;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0)) {
+    for (uint32_t s = 0, ph = 0, it = 0;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0), ++it) {
       mbar_wait(&C.empty_in[s], ph ^ 1u);
       uint32_t t32 = 0;
       if (lane == 0) t32 = atomicAdd(a.ticket, 1u);
+      if (lane == 0) {
+        TRACE(it, 0);
+        TRACE_V(it, 10, t32);
+      }
       const uint64_t t = __shfl_sync(0xffffffffu, t32, 0);
       uint8_t* dst = smem + sh.o_in + (size_t)s * sh.in_stride;
       if (t >= sh.n_tiles) {
@@ -455,21 +568,27 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_compress_pipe(PipeArgs a) 
   }
 
   uint64_t* pay_g = reinterpret_cast<uint64_t*>(a.out + 32 + 16 * sh.n_blocks);
-  if (warp >= W_WRIT && warp < W_WRIT + NWRITERS) {
+  if (warp >= W_WRIT && warp < W_WRIT + (int)a.nlb) {
     // ---------------------------------------------------------- writers
-    // NWRITERS writer warps take records round robin (look-backs overlap);
+    // nlb writer warps take records round robin (look-backs overlap);
     // ring space is released strictly in record order.
-    for (uint32_t i = (uint32_t)(warp - W_WRIT);; i += NWRITERS) {
+    for (uint32_t i = (uint32_t)(warp - W_WRIT);; i += a.nlb) {
       const uint32_t r = i % MAXR, ph = (i / MAXR) & 1u;
       mbar_wait(&C.rec_full[r], ph);
       const uint64_t t = C.rec_t[r];
       if (t == TILE_NONE) break;
+      if (lane == 0) TRACE(i, 5);
       const uint64_t W = C.rec_W[r];
       uint64_t P = 0;
       if (t != 0 && !(a.debug & 2)) {
-        P = lookback_wide(a.status, t);
-        if (lane == 0) st_relaxed_u64(a.status + t, FLAG_PRE | ((P + W) & VAL_MASK));
+        if (a.server) {
+          P = wait_prefix(a.status, t);
+        } else {
+          P = lookback_wide(a.status, t);
+          if (lane == 0) st_relaxed_u64(a.status + t, FLAG_PRE | ((P + W) & VAL_MASK));
+        }
       }
+      if (lane == 0) TRACE(i, 6);
       const uint64_t* src = reinterpret_cast<const uint64_t*>(ring + C.rec_off[r]);
       uint64_t* dst = pay_g + P;
       const uint32_t w = (uint32_t)W;
@@ -488,6 +607,7 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_compress_pipe(PipeArgs a) 
       }
       __syncwarp();
       if (lane == 0) {
+        TRACE(i, 7);
         while (C.wdone != i) __nanosleep(32);
         __threadfence_block();
         C.ring_tail = C.rec_end[r];
@@ -499,20 +619,21 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_compress_pipe(PipeArgs a) 
     return;
   }
 
-  if (warp >= NCW) return;  // spare warp (NWRITERS = 1)
+  if (warp >= NCW) return;  // spare warps
 
   // ------------------------------------------------------------ consumers
   const int ctid = tid;  // 0 .. PC-1
   const uint32_t L = (uint32_t)sh.Le;
   uint4* hdr_g = reinterpret_cast<uint4*>(a.out + 32);
   uint64_t head = 0;  // ring bytes handed out (thread 0's copy is authoritative)
-  for (uint32_t s = 0, ph = 0, r = 0, rph = 0;;
-       s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0), r = (r + 1) % MAXR, rph ^= (r == 0)) {
+  for (uint32_t s = 0, ph = 0, r = 0, rph = 0, it = 0;;
+       s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0), r = (r + 1) % MAXR, rph ^= (r == 0), ++it) {
     mbar_wait(&C.full_in[s], ph);
+    if (ctid == 0) TRACE(it, 1);
     const uint64_t t = C.tkt[s];
     if (t == TILE_NONE) {  // one end marker per writer warp (every consumer warp arrives)
       if (lane == 0) {
-        for (int e = 0; e < NWRITERS; ++e) {
+        for (uint32_t e = 0; e < a.nlb; ++e) {
           mbar_wait(&C.rec_empty[r], rph ^ 1u);
           if (warp == 0) C.rec_t[r] = TILE_NONE;
           mbar_arrive(&C.rec_full[r]);
@@ -598,7 +719,8 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_compress_pipe(PipeArgs a) 
     }
     // ---- a4: publish the tile aggregate, then take ring space for its words
     if (ctid == 0) {
-      st_relaxed_u64(a.status + t, (t == 0 ? FLAG_PRE : FLAG_AGG) | W);
+      st_relaxed_u64(a.status + t, (t == 0 && !a.server ? FLAG_PRE : FLAG_AGG) | W);
+      TRACE(it, 2);
       mbar_wait(&C.rec_empty[r], rph ^ 1u);
       const uint32_t need = (8 * W + 15) & ~15u;
       uint32_t pos = (uint32_t)(head % sh.ring_bytes);
@@ -617,6 +739,7 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_compress_pipe(PipeArgs a) 
       C.rec_W[r] = W;
       C.rec_off[r] = pos;
       C.rec_end[r] = head;
+      TRACE(it, 3);
     }
     cons_bar();
     uint64_t* ow = reinterpret_cast<uint64_t*>(ring + C.rec_off[r]);
@@ -675,6 +798,8 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_compress_pipe(PipeArgs a) 
     // stage free once all NCW warps have arrived (no CTA barrier)
     __syncwarp();
     if (lane == 0) {
+      if (warp == 0) TRACE(it, 4);
+      if (warp == NCW - 1) TRACE(it, 8);
       mbar_arrive(&C.rec_full[r]);
       mbar_arrive(&C.empty_in[s]);
     }
@@ -702,6 +827,130 @@ __device__ __forceinline__ uint32_t check_global_header_p(const PipeArgs& a, uin
   return 0;
 }
 
+// 64-bit fraction step with the block minimum folded into the digit:
+// returns vmin + floor(f B / 2^64), f <- f B mod 2^64 (f = f1:f0).
+__device__ __forceinline__ uint32_t fstep64v(uint32_t& f0, uint32_t& f1, uint32_t B, uint32_t vmin) {
+  uint32_t n0, n1, d;
+  asm("{\n\t.reg .u32 c;\n\t"
+      "mul.lo.u32 %0, %3, %5;\n\t"
+      "mul.hi.u32 c, %3, %5;\n\t"
+      "mad.lo.cc.u32 %1, %4, %5, c;\n\t"
+      "madc.hi.u32 %2, %4, %5, %6;\n\t}"
+      : "=&r"(n0), "=&r"(n1), "=r"(d)
+      : "r"(f0), "r"(f1), "r"(B), "r"(vmin));
+  f0 = n0;
+  f1 = n1;
+  return d;
+}
+// 32-bit step: returns vmin + floor(g B / 2^32), g <- g B mod 2^32.
+__device__ __forceinline__ uint32_t fstep32v(uint32_t& g, uint32_t B, uint32_t vmin) {
+  uint32_t lo, d;
+  asm("mul.lo.u32 %0, %2, %3;\n\tmad.hi.u32 %1, %2, %3, %4;" : "=&r"(lo), "=r"(d) : "r"(g), "r"(B), "r"(vmin));
+  g = lo;
+  return d;
+}
+
+// The m top digits of a word (already premultiplied so they are its top
+// digits), written most significant first at o[0], o[-1], ...: n64 64-bit
+// steps, then n32 32-bit steps.
+template <typename V>
+__device__ __forceinline__ void digits_out(uint32_t f0, uint32_t f1, uint32_t add, uint32_t B, uint32_t vmin,
+                                           int n64, int n32, V* o) {
+#pragma unroll 1
+  for (; n64 >= 2; n64 -= 2, o -= 2) {
+    const uint32_t d1 = fstep64v(f0, f1, B, vmin);
+    const uint32_t d0 = fstep64v(f0, f1, B, vmin);
+    o[0] = (V)d1;
+    o[-1] = (V)d0;
+  }
+  if (n64) {
+    o[0] = (V)fstep64v(f0, f1, B, vmin);
+    --o;
+  }
+  uint32_t g = f1 + add;
+#pragma unroll 1
+  for (; n32 >= 2; n32 -= 2, o -= 2) {
+    const uint32_t d1 = fstep32v(g, B, vmin);
+    const uint32_t d0 = fstep32v(g, B, vmin);
+    o[0] = (V)d1;
+    o[-1] = (V)d0;
+  }
+  if (n32) o[0] = (V)fstep32v(g, B, vmin);
+}
+
+// One full-length block (nb = L, B <= CACHE_B, B < 2^32) from its cached
+// constants: every word decodes exactly its own digits (the top word is
+// premultiplied by P = B^(k - mt), so its k - mt zero digits are skipped and
+// s < B^mt is checked as s P < B^k).
+template <typename V>
+__device__ __forceinline__ uint32_t decode_block_ent(const uint64_t* src, uint32_t nw, uint32_t B, uint32_t vmin,
+                                                     const DecEnt& e, V* dst) {
+  // the constants live in registers for the whole block (the digit stores
+  // would otherwise force the compiler to reload them from shared memory)
+  const uint64_t Rl = e.Rl, Rh = e.Rh, Wmax = e.Wmax, P = e.P;
+  const uint32_t meta = e.meta, mt = e.mt;
+  const uint32_t k = meta & 0xffu, t = (meta >> 16) & 0xffu, add = ((meta >> 8) & 0xffu) ? 0u : 1u;
+  uint32_t err = 0;
+  const uint32_t nfull = mt < k ? nw - 1 : nw;
+  V* o = dst + (k - 1);
+#pragma unroll 1
+  for (uint32_t j = 0; j < nfull; ++j, o += k) {
+    const uint64_t s = src[j];
+    if (s > Wmax) err = POLY_ST_RESIDUE;
+    const uint64_t hi1 = __umul64hi(s, Rl), lo2 = s * Rh, hi2 = __umul64hi(s, Rh), mid = lo2 + hi1;
+    const uint64_t f = ((hi2 + (mid < lo2 ? 1ull : 0ull)) << 32) + (mid >> 32) + add;
+    digits_out<V>((uint32_t)f, (uint32_t)(f >> 32), add, B, vmin, (int)(k - t), (int)t, o);
+  }
+  if (nfull < nw) {  // the top word: mt < k digits, premultiplied by P = B^(k - mt)
+    uint64_t s = src[nfull];
+    if (__umul64hi(s, P) != 0) err = POLY_ST_RESIDUE;
+    s *= P;
+    if (s > Wmax) err = POLY_ST_RESIDUE;
+    const uint64_t hi1 = __umul64hi(s, Rl), lo2 = s * Rh, hi2 = __umul64hi(s, Rh), mid = lo2 + hi1;
+    const uint64_t f = ((hi2 + (mid < lo2 ? 1ull : 0ull)) << 32) + (mid >> 32) + add;
+    const int n32 = (int)(t + mt) > (int)k ? (int)(t + mt - k) : 0;
+    digits_out<V>((uint32_t)f, (uint32_t)(f >> 32), add, B, vmin, (int)mt - n32, n32, dst + (nfull * k + mt - 1));
+  }
+  return err;
+}
+
+// One block of the lane-per-block map (a8, a9): header validation and decode.
+template <typename V>
+__device__ __forceinline__ uint32_t decode_block0(const uint4 h, const uint64_t* src, uint32_t nb, uint32_t L,
+                                                  uint32_t width, const BaseCache& bc, V* dst) {
+  const uint64_t vmax = (width == 16) ? 0xffffull : 0xffffffffull;
+  if (h.x == CODEC_BASIC && h.z != 0 && (uint64_t)h.y + h.z <= vmax) {
+    const uint64_t B = (uint64_t)h.z + 1;
+    if (B <= CACHE_B && nb == L) {
+      const DecEnt& e = bc.E[B];
+      if (h.w != e.nwL) return POLY_ST_NWORDS;
+      return decode_block_ent<V>(src, h.w, (uint32_t)B, h.y, e, dst);
+    }
+  }
+  // general path: partial last block, large bases, constant blocks, errors
+  const uint32_t k = (h.x == CODEC_BASIC && h.z != 0) ? dk_of(bc, (uint64_t)h.z + 1) : 1u;
+  const uint32_t e = check_block_hdr(h, nb, width, k);
+  if (e) return e;
+  if (h.x == CODEC_CONSTANT) {
+    for (uint32_t j = 0; j < nb; ++j) dst[j] = (V)h.y;
+    return 0;
+  }
+  const DecConst c = dconst_of(bc, (uint64_t)h.z + 1);
+  uint32_t err = 0;
+  if (dc_log2b(c) == 32) {  // B = 2^32 (u32 only) does not fit the 32-bit multiplier
+    for (uint32_t j = 0, first = 0; j < h.w; ++j, first += k)
+      err |= decode_pow2<V>(src[j], 32, min(k, nb - first), h.y, dst + first);
+  } else {
+    err = decode_block_lane<V>(src, h.w, nb, c, h.z + 1, h.y, 0ull, dst);
+  }
+  return err;
+}
+
+__device__ __forceinline__ bool check_global_header_p_ok(const PipeArgs& a) {
+  uint64_t pw;
+  return check_global_header_p(a, &pw) == 0;
+}
+
 // The words of a block past its full k-specialised groups (at most Q full
 // words and the top word), one lane each; the top word of a full-length block
 // takes the premultiplied path (m steps, not k).
@@ -713,7 +962,7 @@ __device__ __forceinline__ uint32_t decode_tail(const uint64_t* src, uint32_t j0
   const uint32_t j = j0 + (threadIdx.x & 31);
   if (j < nw) {
     const uint32_t first = j * k, m = min(k, nb - first);
-    const uint64_t P = (m < k && nb == L && B <= CACHE_B) ? bc.P[B] : 0ull;
+    const uint64_t P = (m < k && nb == L && B <= CACHE_B) ? bc.E[B].P : 0ull;
     if (P != 0 && dc_log2b(c) != 32)
       err = decode_top_word<V>(src[j], c, B, m, P, vmin, dst + first);
     else
@@ -725,6 +974,10 @@ __device__ __forceinline__ uint32_t decode_tail(const uint64_t* src, uint32_t j0
 template <typename V, int MAP>
 __global__ void __launch_bounds__(PT, POLY_CTAS) poly_decompress_pipe(PipeArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
+  if (a.server && blockIdx.x == gridDim.x - 1) {
+    if (threadIdx.x < 32 && check_global_header_p_ok(a)) prefix_server(a.status, a.sh.n_tiles);
+    return;
+  }
   PipeCtl& C = *reinterpret_cast<PipeCtl*>(smem);
   const PipeShape& sh = a.sh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -763,6 +1016,8 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_decompress_pipe(PipeArgs a
     for (uint32_t i = 0, s = 0, ph = 0;; ++i) {
       mbar_wait(&C.empty_in[s], ph ^ 1u);
       const uint64_t t = nend ? sh.n_tiles : atomicAdd(a.ticket, 1u);
+      TRACE(i, 0);
+      TRACE_V(i, 10, t);
       if (t >= sh.n_tiles) {
         C.tkt[s] = TILE_NONE;
         mbar_arrive(&C.hbar[s]);
@@ -791,8 +1046,9 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_decompress_pipe(PipeArgs a
     // Publishes each tile's aggregate as soon as its headers land (a7), and
     // the in-tile word offsets of its blocks.
     uint32_t nend = 0;
-    for (uint32_t s = 0, ph = 0;;) {
+    for (uint32_t s = 0, ph = 0, it = 0;; ++it) {
       mbar_wait(&C.hbar[s], ph);
+      if (lane == 0) TRACE(it, 1);
       const uint64_t t = C.tkt[s];
       if (t == TILE_NONE) {
         if (lane == 0) mbar_arrive(&C.aggr[s]);
@@ -808,29 +1064,42 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_decompress_pipe(PipeArgs a
       uint32_t* OFF = reinterpret_cast<uint32_t*>(smem + sh.o_in + (size_t)s * sh.in_stride + sh.o_off);
       const uint64_t b0 = t * sh.TB;
       const uint32_t nblk = (uint32_t)min((uint64_t)sh.TB, sh.n_blocks - b0);
-      // rounds of 32 blocks, lane-strided (bank-conflict free).  map 0: round r is
-      // warp group r of the consumers -> OFF[r] = words before the group; map 1:
-      // OFF[b] = words before block b.  (Offsets of a tile with W > words_cap
-      // are garbage; the look-back warp rejects such a tile.)
+      // OFF[b] = words before block b in the tile: eight independent warp
+      // scans of 32 blocks at a time (their shuffles overlap), then a carry.
+      // A block's n_words is clamped to 2^20 - 1 (a valid block has at most
+      // 4096 words here) so a corrupt header cannot wrap the 32-bit sums; the
+      // consumers reject such a block and the look-back warp such a tile.
       const uint32_t* Hw = reinterpret_cast<const uint32_t*>(H) + 3;
-      uint64_t W = 0;
-      for (uint32_t r0 = 0, rr = 0; r0 < nblk; r0 += 32, ++rr) {
-        const uint32_t b = r0 + lane;
-        const uint32_t x = b < nblk ? Hw[4 * b] : 0u;
-        if (MAP == 0) {
-          if (lane == 0) OFF[rr] = (uint32_t)W;
-          W += warp_sum_u64(x);
-        } else {
-          uint32_t tot;
-          const uint32_t ex = warp_excl_scan(x, &tot);
-          if (b < nblk) OFF[b] = (uint32_t)W + ex;
-          W += warp_sum_u64(x);
+      uint32_t Wt = 0;
+      for (uint32_t r0 = 0; r0 < nblk; r0 += 256) {
+        uint32_t x[8], v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t b = r0 + 32 * q + lane;
+          x[q] = b < nblk ? min(Hw[4 * b], 0xfffffu) : 0u;
+          v[q] = x[q];
+        }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, v[q], o);
+            if (lane >= o) v[q] += y;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t b = r0 + 32 * q + lane;
+          if (b < nblk) OFF[b] = Wt + v[q] - x[q];
+          Wt += __shfl_sync(0xffffffffu, v[q], 31);
         }
       }
+      const uint64_t W = Wt;
       __syncwarp();
       if (lane == 0) {
-        st_relaxed_u64(a.status + t, (t == 0 ? FLAG_PRE : FLAG_AGG) | (W & VAL_MASK));
+        st_relaxed_u64(a.status + t, (t == 0 && !a.server ? FLAG_PRE : FLAG_AGG) | (W & VAL_MASK));
         C.W[s] = W;
+        TRACE(it, 2);
         mbar_arrive(&C.aggr[s]);
       }
       if (++s == S) {
@@ -841,13 +1110,14 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_decompress_pipe(PipeArgs a
     return;
   }
 
-  if (warp == W_WRIT || (warp == W_LB2 && a.nlb == 2)) {
+  const int lbi = warp == W_WRIT ? 0 : (warp >= W_LBX && warp < W_LBX + NLB_MAX - 1) ? warp - W_LBX + 1 : -1;
+  if (lbi >= 0 && lbi < (int)a.nlb) {
     // ---------------------------------------------------------- look-back + payload loader
     // nlb warps take stages round robin, so nlb look-backs are in flight; ring
     // space is handed out strictly in stage order (C.lb_seq).
     const uint64_t pw = C.payload_words;
     const uint32_t nlb = a.nlb;
-    for (uint32_t i = (warp == W_WRIT) ? 0u : 1u;; i += nlb) {
+    for (uint32_t i = (uint32_t)lbi;; i += nlb) {
       const uint32_t s = i % S, ph = (i / S) & 1u;
       mbar_wait(&C.aggr[s], ph);
       const uint64_t t = C.tkt[s];
@@ -855,14 +1125,20 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_decompress_pipe(PipeArgs a
         if (lane == 0) mbar_arrive(&C.full_in[s]);
         break;
       }
+      if (lane == 0) TRACE(i, 3);
       const uint64_t W = C.W[s];
       uint64_t P = 0;
       if (a.debug & 2) {
         P = min(t * (pw / sh.n_tiles), pw - min(pw, W));
       } else if (t != 0) {
-        P = lookback_wide(a.status, t);
-        if (lane == 0) st_relaxed_u64(a.status + t, FLAG_PRE | ((P + W) & VAL_MASK));
+        if (a.server) {
+          P = wait_prefix(a.status, t);
+        } else {
+          P = lookback_wide(a.status, t);
+          if (lane == 0) st_relaxed_u64(a.status + t, FLAG_PRE | ((P + W) & VAL_MASK));
+        }
       }
+      if (lane == 0) TRACE(i, 4);
       uint32_t e = 0;
       uint64_t wl = (a.debug & 16) ? 0 : W;
       if (W > sh.words_cap || P + W > pw) {
@@ -892,6 +1168,7 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_decompress_pipe(PipeArgs a
             __nanosleep(ns);
             ns = ns ? min(ns * 2, 256u) : 32u;
           }
+          TRACE(i, 5);
           __threadfence_block();
           fence_proxy_async_smem();
           uint64_t* dst = reinterpret_cast<uint64_t*>(ring + pos);
@@ -927,8 +1204,10 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_decompress_pipe(PipeArgs a
   const uint32_t L = (uint32_t)sh.Le;
   uint32_t err = 0;
   const bool bst = a.bulk && !(a.debug & 4);
-  for (uint32_t s = 0, ph = 0, s2 = 0;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0), s2 ^= 1u) {
+  for (uint32_t s = 0, ph = 0, s2 = 0, it = 0;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0), s2 ^= 1u, ++it) {
     mbar_wait(&C.full_in[s], ph);
+    if (lane == 0 && warp == 0) TRACE(it, 6);
+    if (lane == 0 && warp == NCW - 1) TRACE(it, 9);
     const uint64_t t = C.tkt[s];
     if (t == TILE_NONE) break;
     const uint8_t* st = smem + sh.o_in + (size_t)s * sh.in_stride;
@@ -953,31 +1232,9 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_decompress_pipe(PipeArgs a
         const uint32_t g0 = q * PC + warp * 32;  // first block of this warp group
         if (g0 >= nblk) break;
         const uint32_t b = g0 + lane;
-        const bool valid = b < nblk;
-        const uint4 h = valid ? H[b] : make_uint4(0, 0, 0, 0);
-        uint32_t tot;
-        const uint32_t ex = warp_excl_scan((valid && !terr) ? h.w : 0u, &tot);
-        if (valid && !terr && !(a.debug & 1)) {
+        if (b < nblk && !terr && !(a.debug & 1)) {
           const uint32_t nb = min(L, nv - b * L);
-          V* dst = ob + (size_t)b * L;
-          const uint32_t k = (h.x == CODEC_BASIC && h.z != 0) ? k_of(bc, (uint64_t)h.z + 1) : 1u;
-          const uint32_t e = check_block_hdr(h, nb, sh.width, k);
-          err |= e;
-          if (!e) {
-            if (h.x == CODEC_CONSTANT) {
-              for (uint32_t j = 0; j < nb; ++j) dst[j] = (V)h.y;
-            } else {
-              const DecConst c = dconst_of(bc, (uint64_t)h.z + 1);
-              const uint64_t* src = PAY + OFF[q * NCW + warp] + ex;
-              if (dc_log2b(c) == 32) {  // B = 2^32 (u32 only) does not fit the 32-bit multiplier
-                for (uint32_t j = 0, first = 0; j < h.w; ++j, first += k)
-                  err |= decode_pow2<V>(src[j], 32, min(k, nb - first), h.y, dst + first);
-              } else {
-                const uint64_t P = (nb == L && h.z + 1 <= CACHE_B) ? bc.P[h.z + 1] : 0ull;
-                err |= decode_block_lane<V>(src, h.w, nb, c, h.z + 1, h.y, P, dst);
-              }
-            }
-          }
+          err |= decode_block0<V>(H[b], PAY + OFF[b], nb, L, sh.width, bc, ob + (size_t)b * L);
         }
         // store the group's 32 blocks (bytes [g0 L vb, min(g0 + 32, nblk) L vb) clipped to nv)
         const uint32_t lo = g0 * L * sh.vb, hi = min(nv, (g0 + 32) * L) * sh.vb;
@@ -1010,7 +1267,7 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_decompress_pipe(PipeArgs a
         uint32_t vlo = (uint32_t)(((uint64_t)nb * part / G) & ~7ull), vhi = part + 1 == G ? nb
                                                                          : (uint32_t)(((uint64_t)nb * (part + 1) / G) & ~7ull);
         if (!terr && !(a.debug & 1)) {
-          const uint32_t k = (h.x == CODEC_BASIC && h.z != 0) ? k_of(bc, (uint64_t)h.z + 1) : 1u;
+          const uint32_t k = (h.x == CODEC_BASIC && h.z != 0) ? dk_of(bc, (uint64_t)h.z + 1) : 1u;
           const uint32_t e = check_block_hdr(h, nb, sh.width, k);
           err |= e;
           if (!e) {
@@ -1066,10 +1323,12 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_decompress_pipe(PipeArgs a
     }
     __syncwarp();
     if (lane == 0) {
+      if (warp == 0) TRACE(it, 7);
       if (bst) bulk_commit();  // one bulk group per warp and tile
       // the last warp done with the stage frees its payload ring space (the
       // stages complete in order: every warp finished the previous one)
       if (atomicAdd(&C.done_cnt[s], 1u) == NCW - 1) {
+        TRACE(it, 8);
         C.done_cnt[s] = 0;
         __threadfence_block();
         C.ring_tail = rend;
