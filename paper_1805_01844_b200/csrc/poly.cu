@@ -15,6 +15,21 @@
 using namespace polyk;
 
 namespace {
+// Consumer warps of the pipeline kernels (compress / decompress).
+// (measured on cfg2/4/5: more warps hide the lane-per-block latency of map 0
+// and of the compress kernels; decompress map 1 is best at 16).
+#ifndef POLY_NCW_C
+#define POLY_NCW_C 24
+#endif
+#ifndef POLY_NCW_D0
+#define POLY_NCW_D0 20
+#endif
+#ifndef POLY_NCW_D1
+#define POLY_NCW_D1 16
+#endif
+constexpr int NCW_C = POLY_NCW_C, NCW_D0 = POLY_NCW_D0, NCW_D1 = POLY_NCW_D1;
+constexpr int pipe_threads(int ncw) { return ncw * 32 + 32 * (2 + NLB_MAX); }
+
 
 enum Regime { LARGE = 1, PIPE = 2, LARGE2 = 3 };
 
@@ -119,14 +134,14 @@ poly_status_t ensure_init(int dev) {
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_dtab, h_dtab, sizeof h_dtab);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
   const int pmax = (POLY_CTAS == 1 ? 227 : 113) * 1024;
-  set_smem_attr(poly_compress_pipe<uint16_t, 0>, pmax);
-  set_smem_attr(poly_compress_pipe<uint16_t, 1>, pmax);
-  set_smem_attr(poly_compress_pipe<uint32_t, 0>, pmax);
-  set_smem_attr(poly_compress_pipe<uint32_t, 1>, pmax);
-  set_smem_attr(poly_decompress_pipe<uint16_t, 0>, pmax);
-  set_smem_attr(poly_decompress_pipe<uint16_t, 1>, pmax);
-  set_smem_attr(poly_decompress_pipe<uint32_t, 0>, pmax);
-  set_smem_attr(poly_decompress_pipe<uint32_t, 1>, pmax);
+  set_smem_attr(poly_compress_pipe<uint16_t, 0, NCW_C>, pmax);
+  set_smem_attr(poly_compress_pipe<uint16_t, 1, NCW_C>, pmax);
+  set_smem_attr(poly_compress_pipe<uint32_t, 0, NCW_C>, pmax);
+  set_smem_attr(poly_compress_pipe<uint32_t, 1, NCW_C>, pmax);
+  set_smem_attr(poly_decompress_pipe<uint16_t, 0, NCW_D0>, pmax);
+  set_smem_attr(poly_decompress_pipe<uint16_t, 1, NCW_D1>, pmax);
+  set_smem_attr(poly_decompress_pipe<uint32_t, 0, NCW_D0>, pmax);
+  set_smem_attr(poly_decompress_pipe<uint32_t, 1, NCW_D1>, pmax);
   set_smem_attr(poly_compress_large<uint16_t>, pmax);
   set_smem_attr(poly_compress_large<uint32_t>, pmax);
   set_smem_attr(poly_decompress_large<uint16_t>, pmax);
@@ -153,6 +168,8 @@ uint32_t r16(uint64_t x) { return (uint32_t)((x + 15) / 16 * 16); }
 
 // Tile shape and shared-memory layout of the pipeline kernels (poly_pipe.cuh).
 bool plan_pipe(const Shape& sh, PipeShape& ps, bool decomp) {
+  const bool map0 = (uint64_t)sh.Le * (sh.width / 8) <= MAP0_MAX_BLOCK;
+  const uint32_t ncw = decomp ? (map0 ? NCW_D0 : NCW_D1) : NCW_C, pc = 32 * ncw;
   memset(&ps, 0, sizeof ps);
   ps.n = sh.n;
   ps.Le = sh.Le;
@@ -164,18 +181,19 @@ bool plan_pipe(const Shape& sh, PipeShape& ps, bool decomp) {
   const uint64_t kmin = sh.width == 16 ? 4 : 2;
   if (bb <= MAP0_MAX_BLOCK) {
     ps.map = 0;
-    uint64_t bpt = PIPE_TILE_TARGET / (PC * bb);
+    uint64_t bpt = PIPE_TILE_TARGET / (pc * bb);
     bpt = std::max<uint64_t>(1, std::min<uint64_t>(BPT_MAX, bpt));
     ps.bpt = (uint32_t)bpt;
-    ps.TB = (uint32_t)(PC * bpt);
+    ps.TB = (uint32_t)(pc * bpt);
   } else {
     ps.map = 1;
     uint64_t tb = PIPE_TILE_TARGET / bb;
     tb = std::max<uint64_t>(1, std::min<uint64_t>(256, tb));
     ps.TB = (uint32_t)tb;
     uint32_t G = 1;
-    while (ps.TB * G * 2 <= (uint32_t)NCW) G *= 2;
+    while (ps.TB * G * 2 <= ncw && ncw % (G * 2) == 0) G *= 2;  // a block's G warps: a whole group
     ps.G = G;
+    ps.TB = std::max<uint32_t>(ps.TB, (ncw + G - 1) / G);  // every consumer warp has a part
     ps.Lp = (uint32_t)(((sh.Le + G - 1) / G + 7) / 8 * 8);
   }
   ps.tile_bytes = (uint32_t)(ps.TB * bb);
@@ -202,8 +220,9 @@ bool plan_pipe(const Shape& sh, PipeShape& ps, bool decomp) {
     ps.o_off = 16 * ps.TB;
     const uint32_t stage = ps.o_off + r16(4ull * ps.TB);
     const uint32_t outb = r16(ps.tile_bytes);
+    // the payload ring (the remainder) holds at least one worst-case tile
     const uint32_t tile_pay = r16(8ull * (ps.words_cap + 2));
-    const int64_t room = (int64_t)PIPE_SMEM_MAX - base - 2 * (int64_t)outb - 2 * (int64_t)tile_pay;
+    const int64_t room = (int64_t)PIPE_SMEM_MAX - base - 2 * (int64_t)outb - (int64_t)tile_pay;
     if (room < 2 * (int64_t)stage) return false;
     ps.S = (uint32_t)std::min<int64_t>(MAXS, room / stage);
     ps.in_stride = stage;
@@ -264,7 +283,7 @@ bool plan(uint64_t n, uint32_t w, uint64_t block_size, Shape& sh, Regime& rg) {
   LargeShape lc, ld;
   if (bb <= PIPE_MAX_BLOCK && plan_pipe(sh, pc, false) && plan_pipe(sh, pd, true)) {
     rg = PIPE;
-    sh.n_chunks = pc.n_tiles;  // tiles (look-back units)
+    sh.n_chunks = std::max(pc.n_tiles, pd.n_tiles);  // tiles (look-back units) of either direction
   } else if (bb <= LARGE2_MAX_BLOCK && sh.n_blocks >= LARGE2_MIN_BLOCKS && plan_large(sh, lc, false) &&
              plan_large(sh, ld, true)) {
     rg = LARGE2;
@@ -323,9 +342,9 @@ uint32_t lb_warps(uint32_t dflt, uint32_t vmax) {
 }
 
 template <typename K>
-int pipe_grid(K kernel, uint32_t smem, uint64_t tiles, int dev) {
+int pipe_grid(K kernel, uint32_t smem, uint64_t tiles, int dev, int threads = PT) {
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, PT, smem) != cudaSuccess || per_sm < 1)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess || per_sm < 1)
     per_sm = 1;
   const uint64_t cap = (uint64_t)(g_sms[dev] > 0 ? g_sms[dev] : 148) * per_sm;
   return (int)std::max<uint64_t>(1, std::min<uint64_t>(cap, tiles));
@@ -334,10 +353,10 @@ int pipe_grid(K kernel, uint32_t smem, uint64_t tiles, int dev) {
 // tile, the prefix-server CTA (all resident: the grid never exceeds what fits).
 // POLY_SERVER=0 selects the in-worker decoupled look-back instead.
 template <typename K>
-int pipe_grid_server(K kernel, uint32_t smem, uint64_t tiles, int dev, uint32_t& server) {
+int pipe_grid_server(K kernel, int threads, uint32_t smem, uint64_t tiles, int dev, uint32_t& server) {
   const char* e = getenv("POLY_SERVER");
   const bool want = !(e && e[0] == '0');
-  const int cap = pipe_grid(kernel, smem, ~0ull, dev);
+  const int cap = pipe_grid(kernel, smem, ~0ull, dev, threads);
   server = (want && tiles > 1 && cap >= 2) ? 1u : 0u;
   const uint64_t workers = std::min<uint64_t>(tiles, (uint64_t)cap - server);
   return (int)(std::max<uint64_t>(1, workers) + server);
@@ -461,10 +480,10 @@ poly_status_t poly_compress(const void* d_in, uint64_t n, poly_dtype_t dt, uint6
     pa.bulk = ((reinterpret_cast<uintptr_t>(d_in) & 15) == 0 && pa.sh.tile_bytes % 16 == 0) ? 1u : 0u;
     pa.debug = debug_flags();
     pa.nlb = lb_warps(2, NLB_MAX + 1);
-    auto k = dt == POLY_U16 ? (pa.sh.map == 0 ? poly_compress_pipe<uint16_t, 0> : poly_compress_pipe<uint16_t, 1>)
-                            : (pa.sh.map == 0 ? poly_compress_pipe<uint32_t, 0> : poly_compress_pipe<uint32_t, 1>);
-    const int grid = pipe_grid_server(k, pa.sh.smem, pa.sh.n_tiles, dev, pa.server);
-    k<<<grid, PT, pa.sh.smem, s>>>(pa);
+    auto k = dt == POLY_U16 ? (pa.sh.map == 0 ? poly_compress_pipe<uint16_t, 0, NCW_C> : poly_compress_pipe<uint16_t, 1, NCW_C>)
+                            : (pa.sh.map == 0 ? poly_compress_pipe<uint32_t, 0, NCW_C> : poly_compress_pipe<uint32_t, 1, NCW_C>);
+    const int grid = pipe_grid_server(k, pipe_threads(NCW_C), pa.sh.smem, pa.sh.n_tiles, dev, pa.server);
+    k<<<grid, pipe_threads(NCW_C), pa.sh.smem, s>>>(pa);
   } else {
     a.bmin = reinterpret_cast<uint32_t*>(ws + W.bmin_off);
     a.bmax = reinterpret_cast<uint32_t*>(ws + W.bmax_off);
@@ -569,10 +588,11 @@ poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_
     // i - nlb, so nlb <= S keeps every parity wait within one phase
     pa.nlb = lb_warps(2, std::min<uint32_t>(NLB_MAX, pa.sh.S));
     auto k = dt == POLY_U16
-                 ? (pa.sh.map == 0 ? poly_decompress_pipe<uint16_t, 0> : poly_decompress_pipe<uint16_t, 1>)
-                 : (pa.sh.map == 0 ? poly_decompress_pipe<uint32_t, 0> : poly_decompress_pipe<uint32_t, 1>);
-    const int grid = pipe_grid_server(k, pa.sh.smem, pa.sh.n_tiles, dev, pa.server);
-    k<<<grid, PT, pa.sh.smem, s>>>(pa);
+                 ? (pa.sh.map == 0 ? poly_decompress_pipe<uint16_t, 0, NCW_D0> : poly_decompress_pipe<uint16_t, 1, NCW_D1>)
+                 : (pa.sh.map == 0 ? poly_decompress_pipe<uint32_t, 0, NCW_D0> : poly_decompress_pipe<uint32_t, 1, NCW_D1>);
+    const int nt = pipe_threads(pa.sh.map == 0 ? NCW_D0 : NCW_D1);
+    const int grid = pipe_grid_server(k, nt, pa.sh.smem, pa.sh.n_tiles, dev, pa.server);
+    k<<<grid, nt, pa.sh.smem, s>>>(pa);
   } else {
     a.woff = reinterpret_cast<uint64_t*>(ws + W.woff_off);
     cudaMemsetAsync(ws, 0, W.bmin_off, s);

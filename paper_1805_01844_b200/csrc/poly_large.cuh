@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_large(LargeArgs a) {
     const uint64_t v0 = (uint64_t)c * sh.SV;
     if (tid == 0 && c == 0) err |= e;
     if (a.bulk && tid == 0) bulk_wait_read<1>();
-    cons_bar();
+    cons_bar<NCW>();
     if (!e) {
       if (h.x == CODEC_CONSTANT) {
         for (uint32_t i = tid; i < nv; i += PC) ob[i] = (V)h.y;
@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_large(LargeArgs a) {
       }
     }
     if (a.bulk) fence_proxy_async_smem();
-    cons_bar();
+    cons_bar<NCW>();
     if (tid == 0) {
       mbar_arrive(&C.empty_in[s]);
       uint8_t* og = a.out + (b * sh.Le + v0) * sh.vb;

@@ -133,7 +133,7 @@ struct __align__(16) PipeCtl {
   uint64_t rec_empty[MAXR];
   uint32_t rec_off[MAXR];
   volatile uint32_t wdone;  // compress: records completed, in order
-  uint32_t scan[2][NCW];
+  uint32_t scan[2][32];      // per consumer warp (NCW <= 32)
   uint64_t payload_words;
   volatile uint64_t ring_tail;  // decompress: ring bytes released by the consumers
   volatile uint32_t lb_seq;     // decompress: next stage to take ring space
@@ -166,8 +166,21 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t tx) {
 #ifndef POLY_SUSPEND_NS
 #define POLY_SUSPEND_NS 0x989680u
 #endif
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity);
+#ifndef POLY_WAIT_BACKOFF
+#define POLY_WAIT_BACKOFF 512  // max sleep (ns) between barrier polls; 0: hardware-suspended try_wait
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-#if POLY_SUSPEND_NS > 0
+#if POLY_WAIT_BACKOFF > 0
+  // Poll with an exponential sleep: a waiting warp (a consumer ahead of the
+  // others, an idle helper) then costs a few issue slots per microsecond
+  // instead of re-polling on every barrier event of the SM.
+  uint32_t ns = 32;
+  while (!mbar_test(bar, parity)) {
+    __nanosleep(ns);
+    ns = min(ns * 2, (uint32_t)POLY_WAIT_BACKOFF);
+  }
+#elif POLY_SUSPEND_NS > 0
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
@@ -222,7 +235,8 @@ __device__ __forceinline__ void bulk_wait_all() {
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-__device__ __forceinline__ void cons_bar() { asm volatile("bar.sync %0, %1;" ::"n"(BAR_CONS), "n"(PC) : "memory"); }
+template <int NW>
+__device__ __forceinline__ void cons_bar() { asm volatile("bar.sync %0, %1;" ::"n"(BAR_CONS), "n"(NW * 32) : "memory"); }
 // Named barrier of the G consecutive warps that share one block (map 1, G > 1).
 __device__ __forceinline__ void group_bar(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -236,14 +250,15 @@ __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t x, uint32_t* total) 
 // Exclusive scan of x over the PC consumer threads; *total = sum.  `buf`
 // alternates between calls (a call's barrier protects the buffer of the
 // call before it).
+template <int NW>
 __device__ __forceinline__ uint32_t cons_scan(uint32_t x, uint32_t* total, uint32_t* buf) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t inc = warp_incl_scan(x);
   if (lane == 31) buf[warp] = inc;
-  cons_bar();
-  const uint32_t ws = lane < NCW ? buf[lane] : 0u;
+  cons_bar<NW>();
+  const uint32_t ws = lane < NW ? buf[lane] : 0u;
   const uint32_t wi = warp_incl_scan(ws);
-  *total = __shfl_sync(0xffffffffu, wi, NCW - 1);
+  *total = __shfl_sync(0xffffffffu, wi, NW - 1);
   const uint32_t wex = __shfl_sync(0xffffffffu, wi - ws, warp);
   return wex + inc - x;
 }
@@ -493,8 +508,12 @@ __device__ __forceinline__ uint64_t wait_prefix(const uint64_t* status, uint64_t
 // ======================================================================
 // compress
 // ======================================================================
-template <typename V, int MAP>
-__global__ void __launch_bounds__(PT, POLY_CTAS) poly_compress_pipe(PipeArgs a) {
+template <typename V, int MAP, int NW>
+__global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_compress_pipe(PipeArgs a) {
+  constexpr int NCW = NW, PC = NW * 32, PT = PC + 32 * (2 + NLB_MAX);
+  constexpr int W_PROD = NCW, W_WRIT = NCW + 1, W_HSUM = NCW + 2, W_LBX = NCW + 3;
+  (void)W_HSUM;
+  (void)W_LBX;
   extern __shared__ __align__(128) uint8_t smem[];
   if (a.server && blockIdx.x == gridDim.x - 1) {
     if (threadIdx.x < 32) prefix_server(a.status, a.sh.n_tiles);
@@ -682,7 +701,7 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_compress_pipe(PipeArgs a) 
             hdr_g[b0 + b] = make_uint4(mx == mn ? CODEC_CONSTANT : CODEC_BASIC, mn, mx - mn, nw[q]);
           }
           uint32_t tot;
-          off[q] = W + cons_scan(nw[q], &tot, C.scan[q & 1]);
+          off[q] = W + cons_scan<NW>(nw[q], &tot, C.scan[q & 1]);
           W += tot;
         }
       }
@@ -699,7 +718,7 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_compress_pipe(PipeArgs a) 
           C.smax[seg] = mx;
         }
       }
-      cons_bar();
+      cons_bar<NW>();
       uint32_t nwb = 0;
       if (ctid < (int)nblk) {
         uint32_t mn = 0xffffffffu, mx = 0u;
@@ -714,7 +733,7 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_compress_pipe(PipeArgs a) 
         C.bnw[ctid] = nwb;
         hdr_g[b0 + ctid] = make_uint4(mx == mn ? CODEC_CONSTANT : CODEC_BASIC, mn, mx - mn, nwb);
       }
-      const uint32_t ex = cons_scan(nwb, &W, C.scan[0]);
+      const uint32_t ex = cons_scan<NW>(nwb, &W, C.scan[0]);
       if (ctid < (int)nblk) C.boff[ctid] = ex;
     }
     // ---- a4: publish the tile aggregate, then take ring space for its words
@@ -741,7 +760,7 @@ __global__ void __launch_bounds__(PT, POLY_CTAS) poly_compress_pipe(PipeArgs a) 
       C.rec_end[r] = head;
       TRACE(it, 3);
     }
-    cons_bar();
+    cons_bar<NW>();
     uint64_t* ow = reinterpret_cast<uint64_t*>(ring + C.rec_off[r]);
 
     // ---- a5: Horner pack
@@ -878,6 +897,49 @@ __device__ __forceinline__ void digits_out(uint32_t f0, uint32_t f1, uint32_t ad
   if (n32) o[0] = (V)fstep32v(g, B, vmin);
 }
 
+#ifndef POLY_PAIR_DECODE
+#define POLY_PAIR_DECODE 0  // 1: decode a block's full words two at a time (measured slower)
+#endif
+// Two full words of one block at once (same B, k, t): the two digit chains
+// interleave, so a lane has two independent multiplies in flight.
+template <typename V>
+__device__ __forceinline__ void digits_out2(uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1, uint32_t add,
+                                            uint32_t B, uint32_t vmin, int n64, int n32, V* oa, V* ob) {
+#pragma unroll 1
+  for (; n64 >= 2; n64 -= 2, oa -= 2, ob -= 2) {
+    const uint32_t x1 = fstep64v(a0, a1, B, vmin);
+    const uint32_t y1 = fstep64v(b0, b1, B, vmin);
+    const uint32_t x0 = fstep64v(a0, a1, B, vmin);
+    const uint32_t y0 = fstep64v(b0, b1, B, vmin);
+    oa[0] = (V)x1;
+    ob[0] = (V)y1;
+    oa[-1] = (V)x0;
+    ob[-1] = (V)y0;
+  }
+  if (n64) {
+    oa[0] = (V)fstep64v(a0, a1, B, vmin);
+    ob[0] = (V)fstep64v(b0, b1, B, vmin);
+    --oa;
+    --ob;
+  }
+  uint32_t ga = a1 + add, gb = b1 + add;
+#pragma unroll 1
+  for (; n32 >= 2; n32 -= 2, oa -= 2, ob -= 2) {
+    const uint32_t x1 = fstep32v(ga, B, vmin);
+    const uint32_t y1 = fstep32v(gb, B, vmin);
+    const uint32_t x0 = fstep32v(ga, B, vmin);
+    const uint32_t y0 = fstep32v(gb, B, vmin);
+    oa[0] = (V)x1;
+    ob[0] = (V)y1;
+    oa[-1] = (V)x0;
+    ob[-1] = (V)y0;
+  }
+  if (n32) {
+    oa[0] = (V)fstep32v(ga, B, vmin);
+    ob[0] = (V)fstep32v(gb, B, vmin);
+  }
+}
+
 // One full-length block (nb = L, B <= CACHE_B, B < 2^32) from its cached
 // constants: every word decodes exactly its own digits (the top word is
 // premultiplied by P = B^(k - mt), so its k - mt zero digits are skipped and
@@ -893,8 +955,22 @@ __device__ __forceinline__ uint32_t decode_block_ent(const uint64_t* src, uint32
   uint32_t err = 0;
   const uint32_t nfull = mt < k ? nw - 1 : nw;
   V* o = dst + (k - 1);
+  uint32_t j = 0;
+#if POLY_PAIR_DECODE
 #pragma unroll 1
-  for (uint32_t j = 0; j < nfull; ++j, o += k) {
+  for (; j + 2 <= nfull; j += 2, o += 2 * k) {  // full words in pairs
+    const uint64_t sa = src[j], sb = src[j + 1];
+    if (sa > Wmax || sb > Wmax) err = POLY_ST_RESIDUE;
+    const uint64_t ha1 = __umul64hi(sa, Rl), la2 = sa * Rh, ha2 = __umul64hi(sa, Rh), ma = la2 + ha1;
+    const uint64_t hb1 = __umul64hi(sb, Rl), lb2 = sb * Rh, hb2 = __umul64hi(sb, Rh), mb = lb2 + hb1;
+    const uint64_t fa = ((ha2 + (ma < la2 ? 1ull : 0ull)) << 32) + (ma >> 32) + add;
+    const uint64_t fb = ((hb2 + (mb < lb2 ? 1ull : 0ull)) << 32) + (mb >> 32) + add;
+    digits_out2<V>((uint32_t)fa, (uint32_t)(fa >> 32), (uint32_t)fb, (uint32_t)(fb >> 32), add, B, vmin,
+                   (int)(k - t), (int)t, o, o + k);
+  }
+#endif
+#pragma unroll 1
+  for (; j < nfull; ++j, o += k) {
     const uint64_t s = src[j];
     if (s > Wmax) err = POLY_ST_RESIDUE;
     const uint64_t hi1 = __umul64hi(s, Rl), lo2 = s * Rh, hi2 = __umul64hi(s, Rh), mid = lo2 + hi1;
@@ -971,8 +1047,12 @@ __device__ __forceinline__ uint32_t decode_tail(const uint64_t* src, uint32_t j0
   return err;
 }
 
-template <typename V, int MAP>
-__global__ void __launch_bounds__(PT, POLY_CTAS) poly_decompress_pipe(PipeArgs a) {
+template <typename V, int MAP, int NW>
+__global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_decompress_pipe(PipeArgs a) {
+  constexpr int NCW = NW, PC = NW * 32, PT = PC + 32 * (2 + NLB_MAX);
+  constexpr int W_PROD = NCW, W_WRIT = NCW + 1, W_HSUM = NCW + 2, W_LBX = NCW + 3;
+  (void)W_HSUM;
+  (void)W_LBX;
   extern __shared__ __align__(128) uint8_t smem[];
   if (a.server && blockIdx.x == gridDim.x - 1) {
     if (threadIdx.x < 32 && check_global_header_p_ok(a)) prefix_server(a.status, a.sh.n_tiles);
