@@ -22,12 +22,16 @@ namespace {
 #define POLY_NCW_C 24
 #endif
 #ifndef POLY_NCW_D0
-#define POLY_NCW_D0 20
+#define POLY_NCW_D0 24
 #endif
 #ifndef POLY_NCW_D1
 #define POLY_NCW_D1 16
 #endif
 constexpr int NCW_C = POLY_NCW_C, NCW_D0 = POLY_NCW_D0, NCW_D1 = POLY_NCW_D1;
+// Decompress header stages (the payload ring gets the rest of shared memory).
+#ifndef POLY_DEC_STAGES
+#define POLY_DEC_STAGES 8
+#endif
 constexpr int pipe_threads(int ncw) { return ncw * 32 + 32 * (2 + NLB_MAX); }
 
 
@@ -219,17 +223,21 @@ bool plan_pipe(const Shape& sh, PipeShape& ps, bool decomp) {
   } else {
     ps.o_off = 16 * ps.TB;
     const uint32_t stage = ps.o_off + r16(4ull * ps.TB);
-    const uint32_t outb = r16(ps.tile_bytes);
+    // staging of the decoded values: map 0, one 32-block group per consumer
+    // warp (copied out right after it is decoded); map 1, two tiles (bulk
+    // stores, the buffer is rewritten two tiles later)
+    const uint32_t outb = ps.map == 0 ? r16(32ull * bb) : r16(ps.tile_bytes);
+    const uint32_t outs = ps.map == 0 ? ncw * outb : 2 * outb;
     // the payload ring (the remainder) holds at least one worst-case tile
     const uint32_t tile_pay = r16(8ull * (ps.words_cap + 2));
-    const int64_t room = (int64_t)PIPE_SMEM_MAX - base - 2 * (int64_t)outb - (int64_t)tile_pay;
+    const int64_t room = (int64_t)PIPE_SMEM_MAX - base - (int64_t)outs - (int64_t)tile_pay;
     if (room < 2 * (int64_t)stage) return false;
-    ps.S = (uint32_t)std::min<int64_t>(MAXS, room / stage);
+    ps.S = (uint32_t)std::min<int64_t>(std::min<int64_t>(MAXS, POLY_DEC_STAGES), room / stage);
     ps.in_stride = stage;
     ps.out_stride = outb;
     ps.o_in = base;
     ps.o_out = base + ps.S * stage;
-    ps.o_ring = ps.o_out + 2 * outb;
+    ps.o_ring = ps.o_out + outs;
     ps.ring_bytes = (PIPE_SMEM_MAX - ps.o_ring) / 16 * 16;
     ps.smem = ps.o_ring + ps.ring_bytes;
   }

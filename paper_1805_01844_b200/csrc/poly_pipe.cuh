@@ -88,7 +88,7 @@ struct PipeShape {
   uint32_t words_cap;   // payload words a tile can hold (any valid stream)
   uint32_t S;           // ring stages (compress input / decompress header stages)
   uint32_t in_stride;   // bytes per stage
-  uint32_t out_stride;  // bytes per staging buffer (two of them)
+  uint32_t out_stride;  // bytes per staging buffer (map 0: per consumer warp; map 1: two per CTA)
   uint32_t o_off;       // decompress: offset of OFF[] inside a header stage (HDR at 0)
   uint32_t o_cache;     // offset of the base-constant cache
   uint32_t o_in, o_out; // offsets of the stages and the staging buffers
@@ -129,6 +129,7 @@ struct __align__(16) PipeCtl {
   uint32_t ring_off[MAXS];  // decompress: byte offset of the stage's payload in the ring
   uint32_t err[MAXS];       // decompress: tile-level status bits
   uint32_t done_cnt[MAXS];  // decompress: warps done with the stage
+  uint32_t gnext[MAXS];     // decompress map 0: next 32-block group of the stage to claim
   uint64_t rec_t[MAXR], rec_W[MAXR], rec_end[MAXR];  // compress: staged tiles
   uint64_t rec_empty[MAXR];
   uint32_t rec_off[MAXR];
@@ -849,17 +850,16 @@ __device__ __forceinline__ uint32_t check_global_header_p(const PipeArgs& a, uin
 // 64-bit fraction step with the block minimum folded into the digit:
 // returns vmin + floor(f B / 2^64), f <- f B mod 2^64 (f = f1:f0).
 __device__ __forceinline__ uint32_t fstep64v(uint32_t& f0, uint32_t& f1, uint32_t B, uint32_t vmin) {
-  uint32_t n0, n1, d;
-  asm("{\n\t.reg .u32 c;\n\t"
-      "mul.lo.u32 %0, %3, %5;\n\t"
-      "mul.hi.u32 c, %3, %5;\n\t"
-      "mad.lo.cc.u32 %1, %4, %5, c;\n\t"
-      "madc.hi.u32 %2, %4, %5, %6;\n\t}"
-      : "=&r"(n0), "=&r"(n1), "=r"(d)
-      : "r"(f0), "r"(f1), "r"(B), "r"(vmin));
+  // (f0 B) gives the new low word and a carry word c; f1 B + (vmin:c) gives
+  // the new high word and vmin + digit (no carry chain across instructions)
+  uint32_t c, n0;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(c) : "r"(f0), "r"(B));
+  asm("mul.lo.u32 %0, %1, %2;" : "=r"(n0) : "r"(f0), "r"(B));
+  uint64_t u;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(u) : "r"(f1), "r"(B), "l"(((uint64_t)vmin << 32) | c));
   f0 = n0;
-  f1 = n1;
-  return d;
+  f1 = (uint32_t)u;
+  return (uint32_t)(u >> 32);
 }
 // 32-bit step: returns vmin + floor(g B / 2^32), g <- g B mod 2^32.
 __device__ __forceinline__ uint32_t fstep32v(uint32_t& g, uint32_t B, uint32_t vmin) {
@@ -875,6 +875,7 @@ __device__ __forceinline__ uint32_t fstep32v(uint32_t& g, uint32_t B, uint32_t v
 template <typename V>
 __device__ __forceinline__ void digits_out(uint32_t f0, uint32_t f1, uint32_t add, uint32_t B, uint32_t vmin,
                                            int n64, int n32, V* o) {
+#if POLY_DIGIT_UNROLL == 2
 #pragma unroll 1
   for (; n64 >= 2; n64 -= 2, o -= 2) {
     const uint32_t d1 = fstep64v(f0, f1, B, vmin);
@@ -895,8 +896,35 @@ __device__ __forceinline__ void digits_out(uint32_t f0, uint32_t f1, uint32_t ad
     o[-1] = (V)d0;
   }
   if (n32) o[0] = (V)fstep32v(g, B, vmin);
+#else
+  // four digits per iteration (the step chains stay in registers), then singles
+#pragma unroll 1
+  for (; n64 >= 4; n64 -= 4, o -= 4) {
+    uint32_t d[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) d[u] = fstep64v(f0, f1, B, vmin);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) o[-u] = (V)d[u];
+  }
+#pragma unroll 1
+  for (; n64 > 0; --n64, --o) o[0] = (V)fstep64v(f0, f1, B, vmin);
+  uint32_t g = f1 + add;
+#pragma unroll 1
+  for (; n32 >= 4; n32 -= 4, o -= 4) {
+    uint32_t d[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) d[u] = fstep32v(g, B, vmin);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) o[-u] = (V)d[u];
+  }
+#pragma unroll 1
+  for (; n32 > 0; --n32, --o) o[0] = (V)fstep32v(g, B, vmin);
+#endif
 }
 
+#ifndef POLY_DIGIT_UNROLL
+#define POLY_DIGIT_UNROLL 2  // digits per iteration of the step loops (2 or 4; 2 measured faster)
+#endif
 #ifndef POLY_PAIR_DECODE
 #define POLY_PAIR_DECODE 0  // 1: decode a block's full words two at a time (measured slower)
 #endif
@@ -1022,6 +1050,8 @@ __device__ __forceinline__ uint32_t decode_block0(const uint4 h, const uint64_t*
   return err;
 }
 
+
+
 __device__ __forceinline__ bool check_global_header_p_ok(const PipeArgs& a) {
   uint64_t pw;
   return check_global_header_p(a, &pw) == 0;
@@ -1071,6 +1101,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       mbar_init(&C.full_in[s], 1);
       mbar_init(&C.empty_in[s], NCW);
       C.done_cnt[s] = 0;
+      C.gnext[s] = 0;
     }
     mbar_fence_init();
     uint64_t pw;
@@ -1151,6 +1182,24 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       // consumers reject such a block and the look-back warp such a tile.
       const uint32_t* Hw = reinterpret_cast<const uint32_t*>(H) + 3;
       uint32_t Wt = 0;
+      if (MAP == 0) {
+        // map 0: only each 32-block group's offset (OFF[g]); a consumer warp
+        // scans within its group.  One warp reduction per group.
+        for (uint32_t r0 = 0; r0 < nblk; r0 += 256) {
+          uint32_t x[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const uint32_t b = r0 + 32 * q + lane;
+            x[q] = b < nblk ? min(Hw[4 * b], 0xfffffu) : 0u;
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const uint32_t sum = __reduce_add_sync(0xffffffffu, x[q]);
+            if (lane == 0 && r0 + 32 * q < nblk) OFF[(r0 >> 5) + q] = Wt;
+            Wt += sum;
+          }
+        }
+      } else
       for (uint32_t r0 = 0; r0 < nblk; r0 += 256) {
         uint32_t x[8], v[8];
 #pragma unroll
@@ -1296,7 +1345,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
     const uint64_t* PAY = reinterpret_cast<const uint64_t*>(ring + C.ring_off[s]) + (C.P[s] & 1);
     const uint32_t terr = C.err[s];
     const uint64_t rend = C.ring_end[s];
-    uint8_t* ob8 = smem + sh.o_out + (size_t)s2 * sh.out_stride;
+    uint8_t* ob8 = smem + sh.o_out + (size_t)(MAP == 0 ? warp : s2) * sh.out_stride;
     V* ob = reinterpret_cast<V*>(ob8);
     const uint64_t b0 = t * sh.TB;
     const uint32_t nblk = (uint32_t)min((uint64_t)sh.TB, sh.n_blocks - b0);
@@ -1304,36 +1353,45 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
     const uint32_t nv = (uint32_t)(min(sh.n, v0 + (uint64_t)sh.TB * sh.Le) - v0);
     uint8_t* og = a.out + v0 * sh.vb;
     if (terr) err |= terr;
-    // this warp's staging regions were last bulk-stored two tiles ago
-    if (bst && lane == 0) bulk_wait_read<1>();
-    __syncwarp();
     if (MAP == 0) {
-      for (uint32_t q = 0; q < sh.bpt; ++q) {
-        const uint32_t g0 = q * PC + warp * 32;  // first block of this warp group
-        if (g0 >= nblk) break;
-        const uint32_t b = g0 + lane;
-        if (b < nblk && !terr && !(a.debug & 1)) {
-          const uint32_t nb = min(L, nv - b * L);
-          err |= decode_block0<V>(H[b], PAY + OFF[b], nb, L, sh.width, bc, ob + (size_t)b * L);
-        }
-        // store the group's 32 blocks (bytes [g0 L vb, min(g0 + 32, nblk) L vb) clipped to nv)
-        const uint32_t lo = g0 * L * sh.vb, hi = min(nv, (g0 + 32) * L) * sh.vb;
-        if (bst) {
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0 && !(a.debug & 8)) {
-            const uint32_t b16 = (hi - lo) & ~15u;  // lo is 16-aligned: 32 L vb is a multiple of 64
-            if (b16) bulk_s2g(og + lo, ob8 + lo, b16);
-            for (uint32_t j = lo + b16; j < hi; ++j) og[j] = ob8[j];
+      // 32-block groups are claimed dynamically, so a warp that is ahead takes
+      // more of the tile and no warp drifts tiles behind the others; each group
+      // is decoded into the warp's own staging buffer and copied out at once.
+      const uint32_t ngrp = (nblk + 31) / 32;
+      const uint32_t gb = 32 * L * sh.vb;  // bytes of a full group (a multiple of 64)
+#pragma unroll 1
+      while (true) {
+        uint32_t g = 0;
+        if (lane == 0) g = atomicAdd(&C.gnext[s], 1u);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        if (g >= ngrp) break;
+        const uint32_t g0 = g * 32, b = g0 + lane;
+        const uint4 h = b < nblk ? H[b] : make_uint4(0, 0, 0, 0);
+        uint32_t tot;
+        const uint32_t ex = warp_excl_scan(min(h.w, 0xfffffu), &tot);
+        if (b < nblk && !terr && !(a.debug & 1))
+          err |= decode_block0<V>(h, PAY + OFF[g] + ex, min(L, nv - b * L), L, sh.width, bc, ob + (size_t)lane * L);
+        __syncwarp();
+        const uint32_t bytes = min(nv * sh.vb - g0 * L * sh.vb, gb);
+        uint8_t* dst = og + (size_t)g0 * L * sh.vb;
+        if (!(a.debug & 8)) {
+          if (a.bulk) {
+            const uint32_t n16 = bytes >> 4;
+            for (uint32_t i = lane; i < n16; i += 32)
+              reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(ob8)[i];
+            for (uint32_t i = 16 * n16 + lane; i < bytes; i += 32) dst[i] = ob8[i];
+          } else {
+            for (uint32_t i = lane; i < bytes; i += 32) dst[i] = ob8[i];
           }
-        } else {
-          __syncwarp();
-          for (uint32_t j = lo + lane; j < hi; j += 32) og[j] = ob8[j];
         }
+        __syncwarp();
       }
     } else {
       // map 1: part p of a block (G parts) decodes and stores one contiguous
-      // range of the block's values, so no warp waits for another
+      // range of the block's values, so no warp waits for another.
+      // This warp's staging regions were last bulk-stored two tiles ago.
+      if (bst && lane == 0) bulk_wait_read<1>();
+      __syncwarp();
       const uint32_t G = sh.G;
       for (uint32_t seg = warp; seg < sh.TB * G; seg += NCW) {
         const uint32_t b = seg / G, part = seg % G;
@@ -1410,6 +1468,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       if (atomicAdd(&C.done_cnt[s], 1u) == NCW - 1) {
         TRACE(it, 8);
         C.done_cnt[s] = 0;
+        C.gnext[s] = 0;
         __threadfence_block();
         C.ring_tail = rend;
       }
