@@ -28,6 +28,13 @@ namespace {
 #define POLY_NCW_D1 16
 #endif
 constexpr int NCW_C = POLY_NCW_C, NCW_D0 = POLY_NCW_D0, NCW_D1 = POLY_NCW_D1;
+// Compress: worst-case tiles the word ring is guaranteed to hold (the input
+// stages get the rest first).  At least 2: a tile's words stay contiguous, so
+// an allocation that wraps skips the ring's tail end (1 tile can deadlock).
+#ifndef POLY_CMP_RING_TILES
+#define POLY_CMP_RING_TILES 2
+#endif
+static_assert(POLY_CMP_RING_TILES >= 2, "the compress word ring needs two worst-case tiles");
 // Decompress header stages (the payload ring gets the rest of shared memory).
 #ifndef POLY_DEC_STAGES
 #define POLY_DEC_STAGES 8
@@ -212,7 +219,7 @@ bool plan_pipe(const Shape& sh, PipeShape& ps, bool decomp) {
     // input ring (S stages) + word ring (the rest, >= 2 worst-case tiles)
     const uint32_t stage = r16(ps.tile_bytes) + 128;  // slack: the top-word pack may read past a block
     const uint32_t tile_words = r16(8ull * ps.words_cap + 16);
-    int64_t room = (int64_t)PIPE_SMEM_MAX - base - 2 * (int64_t)tile_words;
+    int64_t room = (int64_t)PIPE_SMEM_MAX - base - POLY_CMP_RING_TILES * (int64_t)tile_words;
     if (room < 2 * (int64_t)stage) return false;
     ps.S = (uint32_t)std::min<int64_t>(4, room / stage);
     ps.in_stride = stage;
