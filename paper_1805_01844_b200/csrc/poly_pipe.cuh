@@ -168,6 +168,9 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t tx) {
 #define POLY_SUSPEND_NS 0x989680u
 #endif
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity);
+#ifndef POLY_WAIT_MIN
+#define POLY_WAIT_MIN 32  // first sleep (ns) of a barrier poll
+#endif
 #ifndef POLY_WAIT_BACKOFF
 #define POLY_WAIT_BACKOFF 512  // max sleep (ns) between barrier polls; 0: hardware-suspended try_wait
 #endif
@@ -176,7 +179,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   // Poll with an exponential sleep: a waiting warp (a consumer ahead of the
   // others, an idle helper) then costs a few issue slots per microsecond
   // instead of re-polling on every barrier event of the SM.
-  uint32_t ns = 32;
+  uint32_t ns = POLY_WAIT_MIN;
   while (!mbar_test(bar, parity)) {
     __nanosleep(ns);
     ns = min(ns * 2, (uint32_t)POLY_WAIT_BACKOFF);
@@ -869,6 +872,9 @@ __device__ __forceinline__ uint32_t fstep32v(uint32_t& g, uint32_t B, uint32_t v
   return d;
 }
 
+#ifndef POLY_DIGIT_UNROLL
+#define POLY_DIGIT_UNROLL 2  // digits per iteration of the step loops (2 or 4; 2 measured faster)
+#endif
 // The m top digits of a word (already premultiplied so they are its top
 // digits), written most significant first at o[0], o[-1], ...: n64 64-bit
 // steps, then n32 32-bit steps.
@@ -922,9 +928,6 @@ __device__ __forceinline__ void digits_out(uint32_t f0, uint32_t f1, uint32_t ad
 #endif
 }
 
-#ifndef POLY_DIGIT_UNROLL
-#define POLY_DIGIT_UNROLL 2  // digits per iteration of the step loops (2 or 4; 2 measured faster)
-#endif
 #ifndef POLY_PAIR_DECODE
 #define POLY_PAIR_DECODE 0  // 1: decode a block's full words two at a time (measured slower)
 #endif
@@ -1376,9 +1379,13 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
         uint8_t* dst = og + (size_t)g0 * L * sh.vb;
         if (!(a.debug & 8)) {
           if (a.bulk) {
+            // 16-byte copies, lane-strided (a group is at most 4 KiB: <= 8 per lane)
             const uint32_t n16 = bytes >> 4;
-            for (uint32_t i = lane; i < n16; i += 32)
-              reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(ob8)[i];
+            uint4* d4 = reinterpret_cast<uint4*>(dst) + lane;
+            const uint4* s4 = reinterpret_cast<const uint4*>(ob8) + lane;
+#pragma unroll
+            for (uint32_t i = 0; i < 8; ++i)
+              if (lane + 32 * i < n16) d4[32 * i] = s4[32 * i];
             for (uint32_t i = 16 * n16 + lane; i < bytes; i += 32) dst[i] = ob8[i];
           } else {
             for (uint32_t i = lane; i < bytes; i += 32) dst[i] = ob8[i];
