@@ -168,6 +168,9 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t tx) {
 #define POLY_SUSPEND_NS 0x989680u
 #endif
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity);
+#ifndef POLY_MAP0_DYNAMIC
+#define POLY_MAP0_DYNAMIC 1  // decompress map 0: groups claimed from a counter (1) or by warp index (0)
+#endif
 #ifndef POLY_WAIT_MIN
 #define POLY_WAIT_MIN 32  // first sleep (ns) of a barrier poll
 #endif
@@ -1363,10 +1366,14 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       const uint32_t ngrp = (nblk + 31) / 32;
       const uint32_t gb = 32 * L * sh.vb;  // bytes of a full group (a multiple of 64)
 #pragma unroll 1
-      while (true) {
+      for (uint32_t gi = 0;; ++gi) {
         uint32_t g = 0;
+#if POLY_MAP0_DYNAMIC
         if (lane == 0) g = atomicAdd(&C.gnext[s], 1u);
         g = __shfl_sync(0xffffffffu, g, 0);
+#else
+        g = warp + gi * NCW;  // static: group = warp (TB = 32 NCW: one group per warp and tile)
+#endif
         if (g >= ngrp) break;
         const uint32_t g0 = g * 32, b = g0 + lane;
         const uint4 h = b < nblk ? H[b] : make_uint4(0, 0, 0, 0);
