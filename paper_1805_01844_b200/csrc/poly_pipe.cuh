@@ -122,6 +122,7 @@ struct __align__(16) PipeCtl {
   uint64_t full_in[MAXS], empty_in[MAXS];    // stage filled (1 + tx) / released (NCW warps)
   uint64_t hbar[MAXS], aggr[MAXS];           // decompress: headers landed / aggregate published
   uint64_t rec_full[MAXR];    // compress: record ready for the writer
+  uint64_t rec_cnt[MAXR];     // compress WARP_RINGS: every warp's word count of the record known
   uint64_t tkt[MAXS];       // ticket of the tile held by each stage
   uint64_t W[MAXS];         // decompress: payload words of the stage's tile
   uint64_t P[MAXS];         // decompress: payload word prefix of the stage's tile
@@ -141,6 +142,11 @@ struct __align__(16) PipeCtl {
   uint64_t ring_head;           // decompress: ring bytes handed out
   uint32_t hdr_err, pad;
   uint32_t nwL[68];             // compress map 0: ceil(L / k) for k = 1..64
+  // compress map 0 with one block per consumer thread (bpt = 1): per-warp word
+  // rings; record r holds each warp's word count, ring offset and ring end
+  uint32_t rw_words[MAXR][32], rw_off[MAXR][32];
+  uint64_t rw_end[MAXR][32];
+  volatile uint64_t wtail[32];  // per-warp ring bytes released (in record order)
   uint32_t smin[256], smax[256];                        // map 1: partial min / max per segment
   uint32_t bvmin[256], bbm1[256], bnw[256], boff[256];  // map 1: per-block results
 };
@@ -168,6 +174,9 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t tx) {
 #define POLY_SUSPEND_NS 0x989680u
 #endif
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity);
+#ifndef POLY_CMP_WARP_RINGS
+#define POLY_CMP_WARP_RINGS 1  // compress map 0 (bpt = 1): per-warp word rings, no CTA scan
+#endif
 #ifndef POLY_MAP0_DYNAMIC
 #define POLY_MAP0_DYNAMIC 1  // decompress map 0: groups claimed from a counter (1) or by warp index (0)
 #endif
@@ -532,6 +541,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
   const uint32_t S = sh.S;
   const BaseCache bc = cache_at(smem + sh.o_cache, false);
   uint8_t* ring = smem + sh.o_ring;
+  const bool WARP_RINGS = MAP == 0 && sh.bpt == 1 && POLY_CMP_WARP_RINGS;  // see plan_pipe
   if (tid == 0) {
     for (uint32_t s = 0; s < S; ++s) {
       mbar_init(&C.full_in[s], 1);
@@ -539,10 +549,12 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
     }
     for (int r = 0; r < MAXR; ++r) {
       mbar_init(&C.rec_full[r], NCW);
+      mbar_init(&C.rec_cnt[r], NCW);
       mbar_init(&C.rec_empty[r], 1);
     }
     C.ring_tail = 0;
     C.wdone = 0;
+    for (int w = 0; w < 32; ++w) C.wtail[w] = 0;
     mbar_fence_init();
   }
   cache_fill(bc, false);
@@ -600,10 +612,70 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
     // ring space is released strictly in record order.
     for (uint32_t i = (uint32_t)(warp - W_WRIT);; i += a.nlb) {
       const uint32_t r = i % MAXR, ph = (i / MAXR) & 1u;
-      mbar_wait(&C.rec_full[r], ph);
+      mbar_wait(WARP_RINGS ? &C.rec_cnt[r] : &C.rec_full[r], ph);
       const uint64_t t = C.rec_t[r];
       if (t == TILE_NONE) break;
       if (lane == 0) TRACE(i, 5);
+      if (WARP_RINGS) {
+        // the tile's words are NCW warp segments, in warp order
+        const uint32_t ww = lane < NCW ? C.rw_words[r][lane] : 0u;
+        const uint32_t wo = lane < NCW ? C.rw_off[r][lane] : 0u;
+        uint32_t Wt;
+        const uint32_t wex = warp_excl_scan(ww, &Wt);
+        if (lane == 0) st_relaxed_u64(a.status + t, (t == 0 && !a.server ? FLAG_PRE : FLAG_AGG) | Wt);
+        uint64_t P = 0;
+        if (t != 0 && !(a.debug & 2)) {
+          if (a.server) {
+            P = wait_prefix(a.status, t);
+          } else {
+            P = lookback_wide(a.status, t);
+            if (lane == 0) st_relaxed_u64(a.status + t, FLAG_PRE | ((P + Wt) & VAL_MASK));
+          }
+        }
+        if (lane == 0) TRACE(i, 6);
+        mbar_wait(&C.rec_full[r], ph);  // every warp's words packed
+        // copy: each lane walks the tile's words lane-strided; the warp segment
+        // of word j is found by advancing through the (short) segment list
+#pragma unroll 1
+        for (int w = 0; w < NCW; w += 2) {
+          const uint32_t n0 = __shfl_sync(0xffffffffu, ww, w), o0 = __shfl_sync(0xffffffffu, wex, w);
+          const uint32_t s0 = __shfl_sync(0xffffffffu, wo, w);
+          const uint32_t n1 = __shfl_sync(0xffffffffu, ww, w + 1), o1 = __shfl_sync(0xffffffffu, wex, w + 1);
+          const uint32_t s1 = __shfl_sync(0xffffffffu, wo, w + 1);
+          const uint64_t* src0 = reinterpret_cast<const uint64_t*>(ring + (size_t)w * sh.ring_bytes + s0);
+          const uint64_t* src1 = reinterpret_cast<const uint64_t*>(ring + (size_t)(w + 1) * sh.ring_bytes + s1);
+          uint64_t* d0 = pay_g + P + o0;
+          uint64_t* d1 = pay_g + P + o1;
+          const uint32_t nm = max(n0, w + 1 < NCW ? n1 : 0u);
+          for (uint32_t j = lane; j < nm; j += 32) {
+            uint64_t x0 = 0, x1 = 0;
+            if (j < n0) x0 = src0[j];
+            if (w + 1 < NCW && j < n1) x1 = src1[j];
+            if (j < n0) d0[j] = x0;
+            if (w + 1 < NCW && j < n1) d1[j] = x1;
+          }
+        }
+        if (t == sh.n_tiles - 1 && lane == 0) {
+          write_global_header_f(a.out, sh.width, sh.n, sh.block_len, sh.n_blocks, P + Wt);
+          *a.compressed_bytes = 32 + 16 * sh.n_blocks + 8 * (P + Wt);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          TRACE(i, 7);
+          while (C.wdone != i) __nanosleep(32);
+          __threadfence_block();
+        }
+        __syncwarp();
+        if (lane < NCW) C.wtail[lane] = C.rw_end[r][lane];
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_block();
+          C.wdone = i + 1;
+          mbar_arrive(&C.rec_empty[r]);
+        }
+        __syncwarp();
+        continue;
+      }
       const uint64_t W = C.rec_W[r];
       uint64_t P = 0;
       if (t != 0 && !(a.debug & 2)) {
@@ -652,6 +724,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
   const uint32_t L = (uint32_t)sh.Le;
   uint4* hdr_g = reinterpret_cast<uint4*>(a.out + 32);
   uint64_t head = 0;  // ring bytes handed out (thread 0's copy is authoritative)
+  uint64_t whead = 0;  // WARP_RINGS: this warp's ring bytes handed out (lane 0)
   for (uint32_t s = 0, ph = 0, r = 0, rph = 0, it = 0;;
        s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0), r = (r + 1) % MAXR, rph ^= (r == 0), ++it) {
     mbar_wait(&C.full_in[s], ph);
@@ -662,6 +735,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
         for (uint32_t e = 0; e < a.nlb; ++e) {
           mbar_wait(&C.rec_empty[r], rph ^ 1u);
           if (warp == 0) C.rec_t[r] = TILE_NONE;
+          mbar_arrive(&C.rec_cnt[r]);
           mbar_arrive(&C.rec_full[r]);
           r = (r + 1) % MAXR;
           rph ^= (r == 0);
@@ -674,6 +748,72 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
     const uint32_t nblk = (uint32_t)min((uint64_t)sh.TB, sh.n_blocks - b0);
     const uint64_t v0 = b0 * sh.Le;
     const uint32_t nv = (uint32_t)(min(sh.n, v0 + (uint64_t)sh.TB * sh.Le) - v0);
+    if (WARP_RINGS) {
+      // One block per thread; the warp's 32 blocks are packed into its own
+      // word ring -- no CTA scan, no shared ring allocation (the writers
+      // concatenate the warp segments and publish the tile aggregate).
+      const uint32_t b = ctid;
+      uint32_t vmn = 0, bmm = 0, nwb = 0, kkb = 1;
+      if (b < nblk && !(a.debug & 1)) {
+        const uint32_t nb = min(L, nv - b * L);
+        uint32_t mn, mx;
+        block_minmax<V>(sv + (size_t)b * L, nb, mn, mx);
+        vmn = mn;
+        bmm = mx - mn;
+        if (mx != mn) {
+          kkb = sizeof(V) == 2 ? kh_of16(bc, mx - mn + 1) : k_of(bc, (uint64_t)(mx - mn) + 1);
+          nwb = nb == L ? C.nwL[kkb & 0xffu] : ceil_div_small(nb, kkb & 0xffu);
+        }
+        hdr_g[b0 + b] = make_uint4(mx == mn ? CODEC_CONSTANT : CODEC_BASIC, mn, mx - mn, nwb);
+      }
+      uint32_t tot;
+      const uint32_t ex = warp_excl_scan(nwb, &tot);
+      uint32_t pos = 0;
+      if (lane == 0) {
+        mbar_wait(&C.rec_empty[r], rph ^ 1u);
+        const uint32_t need = (8 * tot + 15) & ~15u, RB = sh.ring_bytes;
+        uint32_t p = (uint32_t)(whead % RB);
+        if (p + need > RB) {  // wrap: the segment stays contiguous
+          whead += RB - p;
+          p = 0;
+        }
+        uint32_t ns = 0;
+        while (whead + need - C.wtail[warp] > RB) {
+          __nanosleep(ns);
+          ns = ns ? min(ns * 2, 256u) : 32u;
+        }
+        whead += need;
+        C.rw_off[r][warp] = p;
+        C.rw_words[r][warp] = tot;
+        C.rw_end[r][warp] = whead;
+        if (warp == 0) C.rec_t[r] = t;
+        mbar_arrive(&C.rec_cnt[r]);
+        pos = p;
+        if (warp == 0) TRACE(it, 3);
+      }
+      pos = __shfl_sync(0xffffffffu, pos, 0);
+      uint64_t* ow = reinterpret_cast<uint64_t*>(ring + (size_t)warp * sh.ring_bytes + pos);
+      if (b < nblk && nwb != 0) {
+        const uint32_t nb = min(L, nv - b * L);
+        if (sizeof(V) == 2) {
+          const uint32_t B = bmm + 1, k = kkb & 0xffu, h = kkb >> 8;
+          uint64_t D;
+          uint32_t G;
+          chunk_consts(bc, B, h, D, G);
+          pack_block_lane16(reinterpret_cast<const uint16_t*>(sv + (size_t)b * L), nb, vmn, B, k, h, D, G, nwb,
+                            ow + ex);
+        } else {
+          pack_block_words<V>(sv + (size_t)b * L, nb, vmn, (uint64_t)bmm + 1, kkb, nwb, ow + ex);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        if (warp == 0) TRACE(it, 4);
+        mbar_arrive(&C.rec_full[r]);
+        mbar_arrive(&C.empty_in[s]);
+      }
+      continue;
+    }
     uint32_t W = 0;
     uint32_t vmin[BPT_MAX], bm1[BPT_MAX], nw[BPT_MAX], kk[BPT_MAX], off[BPT_MAX];
 
