@@ -27,7 +27,10 @@ namespace {
 #ifndef POLY_NCW_D1
 #define POLY_NCW_D1 16
 #endif
-constexpr int NCW_C = POLY_NCW_C, NCW_D0 = POLY_NCW_D0, NCW_D1 = POLY_NCW_D1;
+#ifndef POLY_NCW_D1B
+#define POLY_NCW_D1B 12
+#endif
+constexpr int NCW_C = POLY_NCW_C, NCW_D0 = POLY_NCW_D0, NCW_D1 = POLY_NCW_D1, NCW_D1B = POLY_NCW_D1B;
 // Compress: worst-case tiles the word ring is guaranteed to hold (the input
 // stages get the rest first).  At least 2: a tile's words stay contiguous, so
 // an allocation that wraps skips the ring's tail end (1 tile can deadlock).
@@ -151,6 +154,8 @@ poly_status_t ensure_init(int dev) {
   set_smem_attr(poly_compress_pipe<uint32_t, 1, NCW_C>, pmax);
   set_smem_attr(poly_decompress_pipe<uint16_t, 0, NCW_D0>, pmax);
   set_smem_attr(poly_decompress_pipe<uint16_t, 1, NCW_D1>, pmax);
+  set_smem_attr(poly_decompress_pipe<uint16_t, 1, NCW_D1B>, pmax);
+  set_smem_attr(poly_decompress_pipe<uint32_t, 1, NCW_D1B>, pmax);
   set_smem_attr(poly_decompress_pipe<uint32_t, 0, NCW_D0>, pmax);
   set_smem_attr(poly_decompress_pipe<uint32_t, 1, NCW_D1>, pmax);
   set_smem_attr(poly_compress_large<uint16_t>, pmax);
@@ -178,10 +183,10 @@ constexpr uint32_t PIPE_SMEM_MAX = (POLY_CTAS == 1 ? 227 : 113) * 1024;  // shar
 uint32_t r16(uint64_t x) { return (uint32_t)((x + 15) / 16 * 16); }
 
 // Tile shape and shared-memory layout of the pipeline kernels (poly_pipe.cuh).
-bool plan_pipe(const Shape& sh, PipeShape& ps, bool decomp) {
-  const bool map0 = (uint64_t)sh.Le * (sh.width / 8) <= MAP0_MAX_BLOCK;
-  const uint32_t ncw = decomp ? (map0 ? NCW_D0 : NCW_D1) : NCW_C, pc = 32 * ncw;
+bool plan_pipe_n(const Shape& sh, PipeShape& ps, bool decomp, uint32_t ncw) {
+  const uint32_t pc = 32 * ncw;
   memset(&ps, 0, sizeof ps);
+  ps.ncw = ncw;
   ps.n = sh.n;
   ps.Le = sh.Le;
   ps.n_blocks = sh.n_blocks;
@@ -204,7 +209,9 @@ bool plan_pipe(const Shape& sh, PipeShape& ps, bool decomp) {
     uint32_t G = 1;
     while (ps.TB * G * 2 <= ncw && ncw % (G * 2) == 0) G *= 2;  // a block's G warps: a whole group
     ps.G = G;
-    ps.TB = std::max<uint32_t>(ps.TB, (ncw + G - 1) / G);  // every consumer warp has a part
+    // a whole number of segments (block parts) per consumer warp
+    const uint32_t per = std::max<uint32_t>(1, ncw / G);
+    ps.TB = std::max<uint32_t>(per, ps.TB / per * per);
     ps.Lp = (uint32_t)(((sh.Le + G - 1) / G + 7) / 8 * 8);
   }
   ps.tile_bytes = (uint32_t)(ps.TB * bb);
@@ -255,6 +262,25 @@ bool plan_pipe(const Shape& sh, PipeShape& ps, bool decomp) {
     ps.smem = ps.o_ring + ps.ring_bytes;
   }
   return ps.smem <= PIPE_SMEM_MAX;
+}
+
+// Consumer-warp count per kernel: compress NCW_C; decompress map 0 NCW_D0;
+// decompress map 1 the instantiation (NCW_D1 or NCW_D1B) whose plan gives the
+// larger block parts (fewer warps per block: fewer group barriers and part
+// tails), ties to the larger warp count (measured: cfg5 12 warps / 4 KiB
+// parts 1751 GB/s vs 16 / 2 KiB 1439; cfg4 16 warps).
+bool plan_pipe(const Shape& sh, PipeShape& ps, bool decomp) {
+  const bool map0 = (uint64_t)sh.Le * (sh.width / 8) <= MAP0_MAX_BLOCK;
+  if (!decomp) return plan_pipe_n(sh, ps, false, NCW_C);
+  if (map0) return plan_pipe_n(sh, ps, true, NCW_D0);
+  PipeShape a, b;
+  const bool oa = plan_pipe_n(sh, a, true, NCW_D1), ob = plan_pipe_n(sh, b, true, NCW_D1B);
+  if (oa && (!ob || a.G <= b.G)) {
+    ps = a;
+    return true;
+  }
+  ps = b;
+  return ob;
 }
 
 // Large blocks, one CTA per block (poly_large.cuh): sub-tiles of 32 KiB plus a
@@ -612,9 +638,11 @@ poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_
     // i - nlb, so nlb <= S keeps every parity wait within one phase
     pa.nlb = lb_warps(2, std::min<uint32_t>(NLB_MAX, pa.sh.S));
     auto k = dt == POLY_U16
-                 ? (pa.sh.map == 0 ? poly_decompress_pipe<uint16_t, 0, NCW_D0> : poly_decompress_pipe<uint16_t, 1, NCW_D1>)
-                 : (pa.sh.map == 0 ? poly_decompress_pipe<uint32_t, 0, NCW_D0> : poly_decompress_pipe<uint32_t, 1, NCW_D1>);
-    const int nt = pipe_threads(pa.sh.map == 0 ? NCW_D0 : NCW_D1);
+                 ? (pa.sh.map == 0 ? poly_decompress_pipe<uint16_t, 0, NCW_D0>
+                    : pa.sh.ncw == NCW_D1 ? poly_decompress_pipe<uint16_t, 1, NCW_D1> : poly_decompress_pipe<uint16_t, 1, NCW_D1B>)
+                 : (pa.sh.map == 0 ? poly_decompress_pipe<uint32_t, 0, NCW_D0>
+                    : pa.sh.ncw == NCW_D1 ? poly_decompress_pipe<uint32_t, 1, NCW_D1> : poly_decompress_pipe<uint32_t, 1, NCW_D1B>);
+    const int nt = pipe_threads((int)pa.sh.ncw);
     const int grid = pipe_grid_server(k, nt, pa.sh.smem, pa.sh.n_tiles, dev, pa.server);
     k<<<grid, nt, pa.sh.smem, s>>>(pa);
   } else {

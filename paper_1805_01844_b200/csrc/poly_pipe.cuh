@@ -96,7 +96,7 @@ struct PipeShape {
   uint32_t segcap;      // compress: worst-case words of one segment
   uint32_t nslot;       // compress: records in flight (<= MAXR)
   uint32_t slot_bytes;  // compress: bytes of each consumer warp's word ring
-  uint32_t pad3;
+  uint32_t ncw;         // consumer warps of the kernel instantiation this shape is for
   uint32_t smem;        // dynamic shared memory bytes
 };
 
