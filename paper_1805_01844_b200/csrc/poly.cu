@@ -246,8 +246,9 @@ bool plan_pipe_n(const Shape& sh, PipeShape& ps, bool decomp, uint32_t ncw) {
     // staging of the decoded values: map 0, one 32-block group per consumer
     // warp (copied out right after it is decoded); map 1, two tiles (bulk
     // stores, the buffer is rewritten two tiles later)
-    const uint32_t outb = ps.map == 0 ? r16(32ull * bb) : r16(ps.tile_bytes);
-    const uint32_t outs = ps.map == 0 ? ncw * outb : 2 * outb;
+    const bool perwarp = ps.map == 0 || (ps.G == 1 && POLY_MAP1_DYNAMIC);
+    const uint32_t outb = ps.map == 0 ? r16(32ull * bb) : perwarp ? r16(bb) : r16(ps.tile_bytes);
+    const uint32_t outs = perwarp ? ncw * outb : 2 * outb;
     // the payload ring (the remainder) holds at least one worst-case tile
     const uint32_t tile_pay = r16(8ull * (ps.words_cap + 2));
     const int64_t room = (int64_t)PIPE_SMEM_MAX - base - (int64_t)outs - (int64_t)tile_pay;

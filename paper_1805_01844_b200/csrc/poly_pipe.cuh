@@ -174,6 +174,9 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t tx) {
 #define POLY_SUSPEND_NS 0x989680u
 #endif
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity);
+#ifndef POLY_MAP1_DYNAMIC
+#define POLY_MAP1_DYNAMIC 0  // decompress map 1 with G = 1: blocks claimed from a counter, per-warp staging (measured slower on cfg4)
+#endif
 #ifndef POLY_CMP_WARP_RINGS
 #define POLY_CMP_WARP_RINGS 1  // compress map 0 (bpt = 1): per-warp word rings, no CTA scan
 #endif
@@ -1491,7 +1494,8 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
     const uint64_t* PAY = reinterpret_cast<const uint64_t*>(ring + C.ring_off[s]) + (C.P[s] & 1);
     const uint32_t terr = C.err[s];
     const uint64_t rend = C.ring_end[s];
-    uint8_t* ob8 = smem + sh.o_out + (size_t)(MAP == 0 ? warp : s2) * sh.out_stride;
+    const bool dyn1 = MAP == 1 && sh.G == 1 && POLY_MAP1_DYNAMIC;  // whole blocks claimed per warp
+    uint8_t* ob8 = smem + sh.o_out + (size_t)(MAP == 0 || dyn1 ? warp : s2) * sh.out_stride;
     V* ob = reinterpret_cast<V*>(ob8);
     const uint64_t b0 = t * sh.TB;
     const uint32_t nblk = (uint32_t)min((uint64_t)sh.TB, sh.n_blocks - b0);
@@ -1544,10 +1548,21 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       // map 1: part p of a block (G parts) decodes and stores one contiguous
       // range of the block's values, so no warp waits for another.
       // This warp's staging regions were last bulk-stored two tiles ago.
-      if (bst && lane == 0) bulk_wait_read<1>();
-      __syncwarp();
+      // (G = 1: blocks are claimed dynamically, decoded into the warp's own
+      // staging buffer and copied out at once, as in map 0.)
+      if (!dyn1) {
+        if (bst && lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+      }
       const uint32_t G = sh.G;
-      for (uint32_t seg = warp; seg < sh.TB * G; seg += NCW) {
+#pragma unroll 1
+      for (uint32_t gi = 0;; ++gi) {
+        uint32_t seg = warp + gi * NCW;
+        if (dyn1) {
+          if (lane == 0) seg = atomicAdd(&C.gnext[s], 1u);
+          seg = __shfl_sync(0xffffffffu, seg, 0);
+        }
+        if (seg >= sh.TB * G) break;
         const uint32_t b = seg / G, part = seg % G;
         if (b >= nblk) break;
         // the parts' ranges depend on k: every part's bulk store of two tiles
@@ -1555,7 +1570,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
         if (G > 1) group_bar(2 + warp / G, 32 * G);
         const uint4 h = H[b];
         const uint32_t nb = min(L, nv - b * L);
-        V* dst = ob + (size_t)b * L;
+        V* dst = dyn1 ? ob : ob + (size_t)b * L;
         uint32_t vlo = (uint32_t)(((uint64_t)nb * part / G) & ~7ull), vhi = part + 1 == G ? nb
                                                                          : (uint32_t)(((uint64_t)nb * (part + 1) / G) & ~7ull);
         if (!terr && !(a.debug & 1)) {
@@ -1598,6 +1613,24 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
               }
             }
           }
+        }
+        if (dyn1) {  // the whole block: 16-byte copies when the block is 16-byte aligned
+          __syncwarp();
+          const uint32_t bytes = nb * sh.vb;
+          uint8_t* gd = og + (size_t)b * L * sh.vb;
+          if (!(a.debug & 8)) {
+            if (a.bulk && ((L * sh.vb) & 15) == 0) {
+              const uint32_t n16 = bytes >> 4;
+              uint4* d4 = reinterpret_cast<uint4*>(gd);
+              const uint4* s4 = reinterpret_cast<const uint4*>(ob8);
+              for (uint32_t i = lane; i < n16; i += 32) d4[i] = s4[i];
+              for (uint32_t i = 16 * n16 + lane; i < bytes; i += 32) gd[i] = ob8[i];
+            } else {
+              for (uint32_t i = lane; i < bytes; i += 32) gd[i] = ob8[i];
+            }
+          }
+          __syncwarp();
+          continue;
         }
         // store this part's range [vlo, vhi) of block b: bulk interior, plain edges
         const uint32_t lo = (b * L + vlo) * sh.vb, hi = (b * L + vhi) * sh.vb;
