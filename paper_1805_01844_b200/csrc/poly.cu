@@ -22,7 +22,7 @@ namespace {
 #define POLY_NCW_C 24
 #endif
 #ifndef POLY_NCW_D0
-#define POLY_NCW_D0 24
+#define POLY_NCW_D0 26
 #endif
 #ifndef POLY_NCW_D1
 #define POLY_NCW_D1 16
