@@ -232,3 +232,41 @@ def test_empty_input_rejected():
     with pytest.raises(pc.PolyError) as e:
         pc.poly_compress(x, 0)
     assert e.value.code == 2
+
+
+def _pipe_cases():
+    rng = np.random.default_rng(2024)
+    ped = rng.integers(240, 272, 30 * 6000).astype(np.uint16)            # map 0, pedestal-like
+    ped[rng.integers(0, ped.size, 300)] = 2000                            # outlier blocks (more words)
+    return [
+        (ped, 30),
+        (rng.integers(1900, 2100, 1024 * 64).astype(np.uint16), 1024),    # map 1, one warp per block
+        (rng.integers(900, 1100, 4096 * 40).astype(np.uint16), 4096),     # map 1, warp groups per block
+        (rng.integers(0, 70000, 7 * 20011).astype(np.uint32), 7),         # map 0, u32, ragged tail
+    ]
+
+
+@pytest.mark.parametrize("env", [{}, {"POLY_SERVER": "0"}, {"POLY_LB": "1"}, {"POLY_LB": "4"},
+                                 {"POLY_SERVER": "0", "POLY_LB": "3"}])
+def test_prefix_and_warp_variants(oracle_lib, env, monkeypatch):
+    """The tile-prefix variants (prefix-server CTA or in-worker look-back) and
+    the look-back / writer warp counts, read at each launch, give the same
+    bytes."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for x, L in _pipe_cases():
+        check_case(oracle_lib, x, L)
+
+
+def test_repeat_determinism(oracle_lib):
+    """Dynamically claimed groups, per-warp word rings and the prefix server
+    race by design; repeated launches must give the oracle's bytes every time."""
+    cases = _pipe_cases()
+    refs = [oracle_lib.compress(x, L) for x, L in cases]
+    for _ in range(12):
+        for (x, L), ref in zip(cases, refs):
+            s_gpu, y, st = gpu_roundtrip(to_dev(x), L)
+            assert s_gpu == ref
+            assert st == 0
+            assert np.array_equal(y.cpu().view(torch.int16 if x.dtype == np.uint16 else torch.int32)
+                                  .numpy().view(x.dtype), x)
