@@ -514,7 +514,8 @@ poly_status_t poly_compress(const void* d_in, uint64_t n, poly_dtype_t dt, uint6
     la.ticket = a.ticket;
     la.bulk = ((reinterpret_cast<uintptr_t>(d_in) & 15) == 0 && (sh.Le * (dt / 8)) % 16 == 0) ? 1u : 0u;
     auto k = dt == POLY_U16 ? poly_compress_large<uint16_t> : poly_compress_large<uint32_t>;
-    k<<<pipe_grid(k, la.sh.smem, sh.n_blocks, dev), PT, la.sh.smem, s>>>(la);
+    const int grid = pipe_grid_server(k, PT, la.sh.smem, sh.n_blocks, dev, la.server);
+    k<<<grid, PT, la.sh.smem, s>>>(la);
   } else if (rg == PIPE) {
     cudaMemsetAsync(ws, 0, W.total, s);
     PipeArgs pa;
@@ -621,7 +622,8 @@ poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_
     la.ticket = a.ticket;
     la.bulk = ((reinterpret_cast<uintptr_t>(d_out) & 15) == 0 && (sh.Le * (dt / 8)) % 16 == 0) ? 1u : 0u;
     auto k = dt == POLY_U16 ? poly_decompress_large<uint16_t> : poly_decompress_large<uint32_t>;
-    k<<<pipe_grid(k, la.sh.smem, sh.n_blocks, dev), PT, la.sh.smem, s>>>(la);
+    const int grid = pipe_grid_server(k, PT, la.sh.smem, sh.n_blocks, dev, la.server);
+    k<<<grid, PT, la.sh.smem, s>>>(la);
   } else if (rg == PIPE) {
     cudaMemsetAsync(ws, 0, W.total, s);
     PipeArgs pa;

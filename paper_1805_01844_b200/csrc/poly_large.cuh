@@ -46,7 +46,7 @@ struct LargeArgs {
   uint64_t* status;   // look-back words, one per block
   uint32_t* ticket;
   uint32_t bulk;      // value array 16-byte aligned and Le * vb % 16 == 0
-  uint32_t pad;
+  uint32_t server;    // 1: the last CTA is the prefix server (poly_pipe.cuh prefix_server)
   LargeShape sh;
 };
 
@@ -79,6 +79,10 @@ __device__ __forceinline__ uint64_t blk_len(const LargeShape& sh, uint64_t b) {
 template <typename V>
 __global__ void __launch_bounds__(PT, 1) poly_compress_large(LargeArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
+  if (a.server && blockIdx.x == gridDim.x - 1) {
+    if (threadIdx.x < 32) prefix_server(a.status, a.sh.n_blocks);
+    return;
+  }
   LargeCtl& C = *reinterpret_cast<LargeCtl*>(smem);
   const LargeShape& sh = a.sh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -174,8 +178,12 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_large(LargeArgs a) {
       const uint64_t W = C.bnw[bs];
       uint64_t P = 0;
       if (b != 0) {
-        P = lookback_wide(a.status, b);
-        if (lane == 0) st_relaxed_u64(a.status + b, FLAG_PRE | ((P + W) & VAL_MASK));
+        if (a.server) {
+          P = wait_prefix(a.status, b);
+        } else {
+          P = lookback_wide(a.status, b);
+          if (lane == 0) st_relaxed_u64(a.status + b, FLAG_PRE | ((P + W) & VAL_MASK));
+        }
       }
       if (lane == 0) {
         C.bP[bs] = P;
@@ -235,7 +243,7 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_large(LargeArgs a) {
             C.bmin[bs] = 0xffffffffu;  // reset for the block after next
             C.bmax[bs] = 0u;
             C.bcnt[bs] = 0u;
-            st_relaxed_u64(a.status + b, (b == 0 ? FLAG_PRE : FLAG_AGG) | nw);  // a4: aggregate
+            st_relaxed_u64(a.status + b, (b == 0 && !a.server ? FLAG_PRE : FLAG_AGG) | nw);  // a4: aggregate
             mbar_arrive(&C.statsready[bs]);
           }
         }
@@ -305,6 +313,11 @@ __device__ __forceinline__ uint32_t check_global_header_l(const LargeArgs& a, ui
 template <typename V>
 __global__ void __launch_bounds__(PT, 1) poly_decompress_large(LargeArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
+  if (a.server && blockIdx.x == gridDim.x - 1) {
+    uint64_t pw;
+    if (threadIdx.x < 32 && check_global_header_l(a, &pw) == 0) prefix_server(a.status, a.sh.n_blocks);
+    return;
+  }
   LargeCtl& C = *reinterpret_cast<LargeCtl*>(smem);
   const LargeShape& sh = a.sh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -346,11 +359,15 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_large(LargeArgs a) {
       const uint4 h = hdr_g[b];
       const uint64_t nb = blk_len(sh, b);
       const uint64_t W = h.w;
-      if (lane == 0) st_relaxed_u64(a.status + b, (b == 0 ? FLAG_PRE : FLAG_AGG) | (W & VAL_MASK));
+      if (lane == 0) st_relaxed_u64(a.status + b, (b == 0 && !a.server ? FLAG_PRE : FLAG_AGG) | (W & VAL_MASK));
       uint64_t P = 0;
       if (b != 0) {
-        P = lookback_wide(a.status, b);
-        if (lane == 0) st_relaxed_u64(a.status + b, FLAG_PRE | ((P + W) & VAL_MASK));
+        if (a.server) {
+          P = wait_prefix(a.status, b);
+        } else {
+          P = lookback_wide(a.status, b);
+          if (lane == 0) st_relaxed_u64(a.status + b, FLAG_PRE | ((P + W) & VAL_MASK));
+        }
       }
       const uint32_t k = (h.x == CODEC_BASIC && h.z != 0) ? capacity_of((uint64_t)h.z + 1) : 1u;
       uint32_t e = 0;

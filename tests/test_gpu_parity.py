@@ -243,6 +243,7 @@ def _pipe_cases():
         (rng.integers(1900, 2100, 1024 * 64).astype(np.uint16), 1024),    # map 1, one warp per block
         (rng.integers(900, 1100, 4096 * 40).astype(np.uint16), 4096),     # map 1, warp groups per block
         (rng.integers(0, 70000, 7 * 20011).astype(np.uint32), 7),         # map 0, u32, ragged tail
+        (rng.integers(0, 5000, 10000 * 260 + 77).astype(np.uint32), 10000),  # large-block regime
     ]
 
 
