@@ -56,6 +56,7 @@ struct __align__(16) LargeCtl {
   // per stage
   uint64_t sb[MAXS];          // block of the stage (TILE_NONE = end)
   uint32_t spass[MAXS], ssub[MAXS], snv[MAXS], slast[MAXS];
+  uint32_t sseq[MAXS];        // compress: the block's sequence number in this CTA (slot = seq & 1)
   uint64_t sj0[MAXS], sj1[MAXS], sP[MAXS];  // decompress: words of the stage, block payload offset
   uint32_t serr[MAXS];
   uint4 shdr[MAXS];           // decompress: block header
@@ -112,57 +113,68 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_large(LargeArgs a) {
         ph ^= 1u;
       }
     };
-    while (true) {
+    // Order: sweep 0 of block i+1 is issued before sweep 1 of block i, so the
+    // wait for block i's payload offset overlaps the next block's min/max
+    // (block i is still in L2: two blocks per SM fit).
+    auto issue = [&](uint64_t b, uint32_t pass, uint32_t seq) {
+      const uint64_t nb = blk_len(sh, b);
+      const uint32_t nsub = (uint32_t)((nb + sh.SV - 1) / sh.SV);
+      const uint8_t* base = a.in + b * sh.Le * sh.vb;
+      for (uint32_t c = 0; c < nsub; ++c) {
+        mbar_wait(&C.empty_in[s], ph ^ 1u);
+        const uint64_t v0 = (uint64_t)c * sh.SV;
+        const uint32_t nv = (uint32_t)min((uint64_t)sh.SV, nb - v0);
+        const uint32_t halo = pass ? (uint32_t)min((uint64_t)LG_HALO, nb - v0 - nv) : 0u;
+        const uint32_t bytes = (nv + halo) * sh.vb;
+        uint8_t* dst = smem + sh.o_in + (size_t)s * sh.stage;
+        const uint8_t* src = base + v0 * sh.vb;
+        if (a.bulk) {
+          if (lane == 0) {
+            C.sb[s] = b;
+            C.spass[s] = pass;
+            C.ssub[s] = c;
+            C.snv[s] = nv;
+            C.slast[s] = c + 1 == nsub;
+            C.sseq[s] = seq;
+            const uint32_t b16 = bytes & ~15u;
+            for (uint32_t j = b16; j < bytes; ++j) dst[j] = src[j];
+            mbar_arrive_tx(&C.full_in[s], b16);
+            if (b16) bulk_g2s(dst, src, b16, &C.full_in[s]);
+          }
+        } else {
+          warp_copy(dst, src, bytes, lane);
+          __syncwarp();
+          if (lane == 0) {
+            C.sb[s] = b;
+            C.spass[s] = pass;
+            C.ssub[s] = c;
+            C.snv[s] = nv;
+            C.slast[s] = c + 1 == nsub;
+            C.sseq[s] = seq;
+            mbar_arrive(&C.full_in[s]);
+          }
+        }
+        next();
+      }
+    };
+    uint64_t prev = TILE_NONE;
+    for (uint32_t seq = 0;; ++seq) {
       uint32_t t32 = 0;
       if (lane == 0) t32 = atomicAdd(a.ticket, 1u);
       const uint64_t b = __shfl_sync(0xffffffffu, t32, 0);
-      if (b >= sh.n_blocks) {
+      const bool more = b < sh.n_blocks;
+      if (more) issue(b, 0, seq);
+      if (prev != TILE_NONE) issue(prev, 1, seq - 1);
+      if (!more) {
         mbar_wait(&C.empty_in[s], ph ^ 1u);
         if (lane == 0) {
           C.sb[s] = TILE_NONE;
+          C.sseq[s] = seq;  // the writer's end marker goes to slot seq & 1
           mbar_arrive(&C.full_in[s]);
         }
         break;
       }
-      const uint64_t nb = blk_len(sh, b);
-      const uint32_t nsub = (uint32_t)((nb + sh.SV - 1) / sh.SV);
-      const uint8_t* base = a.in + b * sh.Le * sh.vb;
-      for (uint32_t pass = 0; pass < 2; ++pass) {
-        for (uint32_t c = 0; c < nsub; ++c) {
-          mbar_wait(&C.empty_in[s], ph ^ 1u);
-          const uint64_t v0 = (uint64_t)c * sh.SV;
-          const uint32_t nv = (uint32_t)min((uint64_t)sh.SV, nb - v0);
-          const uint32_t halo = pass ? (uint32_t)min((uint64_t)LG_HALO, nb - v0 - nv) : 0u;
-          const uint32_t bytes = (nv + halo) * sh.vb;
-          uint8_t* dst = smem + sh.o_in + (size_t)s * sh.stage;
-          const uint8_t* src = base + v0 * sh.vb;
-          if (a.bulk) {
-            if (lane == 0) {
-              C.sb[s] = b;
-              C.spass[s] = pass;
-              C.ssub[s] = c;
-              C.snv[s] = nv;
-              C.slast[s] = c + 1 == nsub;
-              const uint32_t b16 = bytes & ~15u;
-              for (uint32_t j = b16; j < bytes; ++j) dst[j] = src[j];
-              mbar_arrive_tx(&C.full_in[s], b16);
-              if (b16) bulk_g2s(dst, src, b16, &C.full_in[s]);
-            }
-          } else {
-            warp_copy(dst, src, bytes, lane);
-            __syncwarp();
-            if (lane == 0) {
-              C.sb[s] = b;
-              C.spass[s] = pass;
-              C.ssub[s] = c;
-              C.snv[s] = nv;
-              C.slast[s] = c + 1 == nsub;
-              mbar_arrive(&C.full_in[s]);
-            }
-          }
-          next();
-        }
-      }
+      prev = b;
     }
     return;
   }
@@ -201,13 +213,13 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_large(LargeArgs a) {
 
   // ------------------------------------------------------------ consumers
   uint4* hdr_g = reinterpret_cast<uint4*>(a.out + 32);
-  uint32_t iblk = 0;  // blocks started (sweep 0, sub-tile 0) by this CTA
   for (uint32_t s = 0, ph = 0;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0)) {
     mbar_wait(&C.full_in[s], ph);
     const uint64_t b = C.sb[s];
+    const uint32_t seq = C.sseq[s];
     if (b == TILE_NONE) {
       if (warp == 0 && lane == 0) {  // end marker for the writer
-        const uint32_t bs = iblk & 1u;
+        const uint32_t bs = seq & 1u;
         C.blk[bs] = TILE_NONE;
         mbar_arrive(&C.statsready[bs]);
       }
@@ -217,7 +229,7 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_large(LargeArgs a) {
     const V* sv = reinterpret_cast<const V*>(smem + sh.o_in + (size_t)s * sh.stage);
     const uint32_t nb = (uint32_t)blk_len(sh, b);  // < 2^24 (block <= 4 MiB)
     if (pass == 0) {
-      const uint32_t bs = iblk & 1u;
+      const uint32_t bs = seq & 1u;
       // ---- a2: min / max of the sub-tile, warp slices, folded into the block's
       const uint32_t per = ((nv + NCW - 1) / NCW + 7) & ~7u;
       const uint32_t lo = min(nv, warp * per), hi = min(nv, lo + per);
@@ -248,11 +260,10 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_large(LargeArgs a) {
           }
         }
       }
-      if (last) ++iblk;
     } else {
       // ---- a5: words whose first value lies in this sub-tile, straight to HBM
-      const uint32_t bs = (iblk - 1) & 1u;  // the block of sweep 1 is the last one started
-      mbar_wait(&C.prefixready[bs], ((iblk - 1) >> 1) & 1u);
+      const uint32_t bs = seq & 1u;
+      mbar_wait(&C.prefixready[bs], (seq >> 1) & 1u);
       const uint32_t bm1 = C.bbm1[bs];
       if (bm1 != 0) {
         const uint32_t vmin = C.bvmin[bs], k = C.bk[bs];
