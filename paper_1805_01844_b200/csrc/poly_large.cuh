@@ -355,10 +355,24 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_large(LargeArgs a) {
     // ---------------------------------------------------------- scheduler
     const uint64_t pw = C.payload_words;
     uint32_t s = 0, ph = 0;
-    while (true) {
+    // One block ahead: the next block's ticket is taken and its aggregate
+    // published before this block waits for its payload offset, so the
+    // prefix frontier never waits on a scheduler that is itself waiting.
+    auto take = [&](uint4& hh) -> uint64_t {
       uint32_t t32 = 0;
       if (lane == 0) t32 = atomicAdd(a.ticket, 1u);
-      const uint64_t b = __shfl_sync(0xffffffffu, t32, 0);
+      const uint64_t bb = __shfl_sync(0xffffffffu, t32, 0);
+      if (bb < sh.n_blocks) {
+        hh = hdr_g[bb];
+        if (lane == 0) st_relaxed_u64(a.status + bb, (bb == 0 && !a.server ? FLAG_PRE : FLAG_AGG) | (hh.w & VAL_MASK));
+      }
+      return bb;
+    };
+    uint4 hn = make_uint4(0, 0, 0, 0);
+    uint64_t bn = take(hn);
+    while (true) {
+      const uint64_t b = bn;
+      const uint4 h = hn;
       if (b >= sh.n_blocks) {
         if (lane == 0) {
           mbar_wait(&C.empty_in[s], ph ^ 1u);
@@ -367,10 +381,9 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_large(LargeArgs a) {
         }
         break;
       }
-      const uint4 h = hdr_g[b];
+      bn = take(hn);
       const uint64_t nb = blk_len(sh, b);
       const uint64_t W = h.w;
-      if (lane == 0) st_relaxed_u64(a.status + b, (b == 0 && !a.server ? FLAG_PRE : FLAG_AGG) | (W & VAL_MASK));
       uint64_t P = 0;
       if (b != 0) {
         if (a.server) {
