@@ -68,6 +68,11 @@ struct __align__(16) LargeCtl {
   uint64_t bP[2];
   uint64_t payload_words;
   uint32_t hdr_err, pad;
+  // decompress: staging buffers (two) filled by the consumer warps (count NCW)
+  // and freed by the store warp once its bulk store has read them
+  uint64_t sfull[2], sfree[2];
+  uint8_t* st_og[2];          // destination of the staging buffer's values
+  uint32_t st_bytes[2];       // bytes (~0u: end of the stream)
 };
 
 __device__ __forceinline__ uint64_t blk_len(const LargeShape& sh, uint64_t b) {
@@ -336,7 +341,11 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_large(LargeArgs a) {
   if (tid == 0) {
     for (uint32_t s = 0; s < S; ++s) {
       mbar_init(&C.full_in[s], 1);
-      mbar_init(&C.empty_in[s], 1);
+      mbar_init(&C.empty_in[s], NCW);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&C.sfull[q], NCW);
+      mbar_init(&C.sfree[q], 1);
     }
     mbar_fence_init();
     uint64_t pw;
@@ -351,6 +360,34 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_large(LargeArgs a) {
   const uint4* hdr_g = reinterpret_cast<const uint4*>(a.in + 32);
   const uint64_t* pay_g = reinterpret_cast<const uint64_t*>(a.in + 32 + 16 * sh.n_blocks);
 
+  if (warp == W_PROD) {
+    // ---------------------------------------------------------- store warp
+    // Bulk-stores each staging buffer once every consumer warp has filled it,
+    // then frees it: the consumers never wait for one another.
+    for (uint32_t i = 0;; ++i) {
+      const uint32_t q = i & 1u;
+      mbar_wait(&C.sfull[q], (i >> 1) & 1u);
+      const uint32_t bytes = C.st_bytes[q];
+      if (bytes == ~0u) break;
+      uint8_t* og = C.st_og[q];
+      const uint8_t* src = smem + sh.o_out + (size_t)q * sh.SV * sh.vb;
+      if (a.bulk) {
+        const uint32_t b16 = bytes & ~15u;
+        if (lane == 0 && b16) bulk_s2g(og, src, b16);
+        for (uint32_t j = b16 + lane; j < bytes; j += 32) og[j] = src[j];
+        if (lane == 0) {
+          bulk_commit();
+          bulk_wait_read<0>();
+        }
+      } else {
+        for (uint32_t j = lane; j < bytes; j += 32) og[j] = src[j];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&C.sfree[q]);
+    }
+    if (a.bulk && lane == 0) bulk_wait_all<0>();
+    return;
+  }
   if (warp == W_WRIT) {
     // ---------------------------------------------------------- scheduler
     const uint64_t pw = C.payload_words;
@@ -455,10 +492,17 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_large(LargeArgs a) {
 
   // ------------------------------------------------------------ consumers
   uint32_t err = 0;
-  for (uint32_t s = 0, ph = 0, s2 = 0;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0), s2 ^= 1u) {
+  for (uint32_t s = 0, ph = 0, i = 0;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0), ++i) {
+    const uint32_t s2 = i & 1u;
     mbar_wait(&C.full_in[s], ph);
     const uint64_t b = C.sb[s];
-    if (b == TILE_NONE) break;
+    if (b == TILE_NONE) {
+      mbar_wait(&C.sfree[s2], ((i >> 1) & 1u) ^ 1u);
+      if (tid == 0) C.st_bytes[s2] = ~0u;  // end marker for the store warp
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&C.sfull[s2]);
+      break;
+    }
     const uint32_t c = C.ssub[s], nv = C.snv[s], e = C.serr[s];
     const uint64_t j0 = C.sj0[s], j1 = C.sj1[s];
     const uint4 h = C.shdr[s];
@@ -467,11 +511,10 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_large(LargeArgs a) {
     const uint64_t nb = blk_len(sh, b);
     const uint64_t v0 = (uint64_t)c * sh.SV;
     if (tid == 0 && c == 0) err |= e;
-    if (a.bulk && tid == 0) bulk_wait_read<1>();
-    cons_bar<NCW>();
+    mbar_wait(&C.sfree[s2], ((i >> 1) & 1u) ^ 1u);  // the buffer's store of two sub-tiles ago has read it
     if (!e) {
       if (h.x == CODEC_CONSTANT) {
-        for (uint32_t i = tid; i < nv; i += PC) ob[i] = (V)h.y;
+        for (uint32_t i2 = tid; i2 < nv; i2 += PC) ob[i2] = (V)h.y;
       } else {
         const DecConst dc = C.sdc[s];
         const uint32_t k = dc_k(dc);
@@ -484,34 +527,25 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_large(LargeArgs a) {
           } else {  // crosses a sub-tile edge: decode to scratch, keep the part inside
             V tmp[64];
             err |= decode_any<V>(words[jj], dc, h.z, m, h.y, tmp);
-            for (uint32_t i = 0; i < m; ++i) {
-              const uint32_t p = first + i;
-              if (p >= v032 && p < v032 + nv) ob[p - v032] = tmp[i];
+            for (uint32_t q = 0; q < m; ++q) {
+              const uint32_t p = first + q;
+              if (p >= v032 && p < v032 + nv) ob[p - v032] = tmp[q];
             }
           }
         }
       }
     }
     if (a.bulk) fence_proxy_async_smem();
-    cons_bar<NCW>();
     if (tid == 0) {
+      C.st_og[s2] = a.out + (b * sh.Le + v0) * sh.vb;
+      C.st_bytes[s2] = nv * sh.vb;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&C.sfull[s2]);
       mbar_arrive(&C.empty_in[s]);
-      uint8_t* og = a.out + (b * sh.Le + v0) * sh.vb;
-      const uint8_t* src = reinterpret_cast<const uint8_t*>(ob);
-      const uint32_t bytes = nv * sh.vb;
-      if (a.bulk) {
-        const uint32_t b16 = bytes & ~15u;
-        if (b16) {
-          bulk_s2g(og, src, b16);
-          bulk_commit();
-        }
-        for (uint32_t j = b16; j < bytes; ++j) og[j] = src[j];
-      } else {
-        for (uint32_t j = 0; j < bytes; ++j) og[j] = src[j];
-      }
     }
   }
-  if (a.bulk && tid == 0) bulk_wait_all<0>();
   err = __reduce_or_sync(0xffffffffu, err);
   if (lane == 0 && err) atomicOr(a.status_out, err);
 }
