@@ -246,7 +246,7 @@ bool plan_pipe_n(const Shape& sh, PipeShape& ps, bool decomp, uint32_t ncw) {
     // staging of the decoded values: map 0, one 32-block group per consumer
     // warp (copied out right after it is decoded); map 1, two tiles (bulk
     // stores, the buffer is rewritten two tiles later)
-    const bool perwarp = ps.map == 0 || (ps.G == 1 && POLY_MAP1_DYNAMIC);
+    const bool perwarp = ps.map == 0;
     const uint32_t outb = ps.map == 0 ? r16(32ull * bb) : perwarp ? r16(bb) : r16(ps.tile_bytes);
     const uint32_t outs = perwarp ? ncw * outb : 2 * outb;
     // the payload ring (the remainder) holds at least one worst-case tile
@@ -639,7 +639,8 @@ poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_
     pa.debug = debug_flags();
     // a look-back warp waits on stage i's barrier only after finishing stage
     // i - nlb, so nlb <= S keeps every parity wait within one phase
-    pa.nlb = lb_warps(2, std::min<uint32_t>(NLB_MAX, pa.sh.S));
+    // (map 1: the last helper warp is the tile store warp)
+    pa.nlb = lb_warps(2, std::min<uint32_t>(pa.sh.map == 1 ? NLB_MAX - 1 : NLB_MAX, pa.sh.S));
     auto k = dt == POLY_U16
                  ? (pa.sh.map == 0 ? poly_decompress_pipe<uint16_t, 0, NCW_D0>
                     : pa.sh.ncw == NCW_D1 ? poly_decompress_pipe<uint16_t, 1, NCW_D1> : poly_decompress_pipe<uint16_t, 1, NCW_D1B>)

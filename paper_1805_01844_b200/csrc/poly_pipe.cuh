@@ -130,7 +130,10 @@ struct __align__(16) PipeCtl {
   uint32_t ring_off[MAXS];  // decompress: byte offset of the stage's payload in the ring
   uint32_t err[MAXS];       // decompress: tile-level status bits
   uint32_t done_cnt[MAXS];  // decompress: warps done with the stage
-  uint32_t gnext[MAXS];     // decompress map 0: next 32-block group of the stage to claim
+  uint32_t gnext[MAXS];     // decompress: next group (map 0) / block (map 1, G = 1) of the stage to claim
+  uint64_t tfull[2], tfree[2];  // decompress map 1: staging tile filled (NCW warps) / read by its bulk store
+  uint8_t* t_og[2];             // decompress map 1: destination of the staging tile
+  uint32_t t_bytes[2];          // decompress map 1: its bytes (~0u: end)
   uint64_t rec_t[MAXR], rec_W[MAXR], rec_end[MAXR];  // compress: staged tiles
   uint64_t rec_empty[MAXR];
   uint32_t rec_off[MAXR];
@@ -174,8 +177,8 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t tx) {
 #define POLY_SUSPEND_NS 0x989680u
 #endif
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity);
-#ifndef POLY_MAP1_DYNAMIC
-#define POLY_MAP1_DYNAMIC 0  // decompress map 1 with G = 1: blocks claimed from a counter, per-warp staging (measured slower on cfg4)
+#ifndef POLY_MAP1_CLAIM
+#define POLY_MAP1_CLAIM 0  // decompress map 1 with G = 1: blocks claimed from a counter (measured slower)
 #endif
 #ifndef POLY_CMP_WARP_RINGS
 #define POLY_CMP_WARP_RINGS 1  // compress map 0 (bpt = 1): per-warp word rings, no CTA scan
@@ -1252,6 +1255,10 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       C.done_cnt[s] = 0;
       C.gnext[s] = 0;
     }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&C.tfull[q], NCW);
+      mbar_init(&C.tfree[q], 1);
+    }
     mbar_fence_init();
     uint64_t pw;
     C.hdr_err = check_global_header_p(a, &pw);
@@ -1472,6 +1479,36 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
     }
     return;
   }
+  if (MAP == 1 && warp == NCW + 1 + NLB_MAX) {
+    // ---------------------------------------------------------- tile store warp (map 1)
+    // One bulk store per decoded tile, issued once every consumer warp has
+    // filled its parts; the staging tile is freed when the store has read it.
+    for (uint32_t i = 0;; ++i) {
+      const uint32_t q = i & 1u;
+      mbar_wait(&C.tfull[q], (i >> 1) & 1u);
+      const uint32_t bytes = C.t_bytes[q];
+      if (bytes == ~0u) break;
+      uint8_t* og = C.t_og[q];
+      const uint8_t* src = smem + sh.o_out + (size_t)q * sh.out_stride;
+      if (bytes && !(a.debug & 8)) {
+        if (a.bulk) {
+          const uint32_t b16 = bytes & ~15u;  // the tile starts 16-byte aligned
+          if (lane == 0 && b16) bulk_s2g(og, src, b16);
+          for (uint32_t j = b16 + lane; j < bytes; j += 32) og[j] = src[j];
+          if (lane == 0) {
+            bulk_commit();
+            bulk_wait_read<0>();
+          }
+        } else {
+          for (uint32_t j = lane; j < bytes; j += 32) og[j] = src[j];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&C.tfree[q]);
+    }
+    if (a.bulk && lane == 0) bulk_wait_all<0>();
+    return;
+  }
   if (warp >= NCW) return;  // spare warps
 
   // ------------------------------------------------------------ consumers
@@ -1487,15 +1524,22 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
     if (lane == 0 && warp == 0) TRACE(it, 6);
     if (lane == 0 && warp == NCW - 1) TRACE(it, 9);
     const uint64_t t = C.tkt[s];
-    if (t == TILE_NONE) break;
+    if (t == TILE_NONE) {
+      if (MAP == 1) {  // end marker for the tile store warp
+        mbar_wait(&C.tfree[s2], ((it >> 1) & 1u) ^ 1u);
+        if (warp == 0 && lane == 0) C.t_bytes[s2] = ~0u;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&C.tfull[s2]);
+      }
+      break;
+    }
     const uint8_t* st = smem + sh.o_in + (size_t)s * sh.in_stride;
     const uint4* H = reinterpret_cast<const uint4*>(st);
     const uint32_t* OFF = reinterpret_cast<const uint32_t*>(st + sh.o_off);
     const uint64_t* PAY = reinterpret_cast<const uint64_t*>(ring + C.ring_off[s]) + (C.P[s] & 1);
     const uint32_t terr = C.err[s];
     const uint64_t rend = C.ring_end[s];
-    const bool dyn1 = MAP == 1 && sh.G == 1 && POLY_MAP1_DYNAMIC;  // whole blocks claimed per warp
-    uint8_t* ob8 = smem + sh.o_out + (size_t)(MAP == 0 || dyn1 ? warp : s2) * sh.out_stride;
+    uint8_t* ob8 = smem + sh.o_out + (size_t)(MAP == 0 ? warp : s2) * sh.out_stride;
     V* ob = reinterpret_cast<V*>(ob8);
     const uint64_t b0 = t * sh.TB;
     const uint32_t nblk = (uint32_t)min((uint64_t)sh.TB, sh.n_blocks - b0);
@@ -1545,32 +1589,26 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
         __syncwarp();
       }
     } else {
-      // map 1: part p of a block (G parts) decodes and stores one contiguous
-      // range of the block's values, so no warp waits for another.
-      // This warp's staging regions were last bulk-stored two tiles ago.
-      // (G = 1: blocks are claimed dynamically, decoded into the warp's own
-      // staging buffer and copied out at once, as in map 0.)
-      if (!dyn1) {
-        if (bst && lane == 0) bulk_wait_read<1>();
-        __syncwarp();
-      }
+      // map 1: part p of a block (G parts) decodes one contiguous range of the
+      // block's values into the tile's staging buffer; the tile store warp
+      // bulk-stores the whole tile once every warp is done, so no warp waits
+      // for another (the buffer was freed by the store of two tiles ago).
+      mbar_wait(&C.tfree[s2], ((it >> 1) & 1u) ^ 1u);
+      const bool claim = sh.G == 1 && POLY_MAP1_CLAIM;
       const uint32_t G = sh.G;
 #pragma unroll 1
       for (uint32_t gi = 0;; ++gi) {
         uint32_t seg = warp + gi * NCW;
-        if (dyn1) {
+        if (claim) {
           if (lane == 0) seg = atomicAdd(&C.gnext[s], 1u);
           seg = __shfl_sync(0xffffffffu, seg, 0);
         }
         if (seg >= sh.TB * G) break;
         const uint32_t b = seg / G, part = seg % G;
         if (b >= nblk) break;
-        // the parts' ranges depend on k: every part's bulk store of two tiles
-        // ago has finished reading (waited above) before any part rewrites
-        if (G > 1) group_bar(2 + warp / G, 32 * G);
         const uint4 h = H[b];
         const uint32_t nb = min(L, nv - b * L);
-        V* dst = dyn1 ? ob : ob + (size_t)b * L;
+        V* dst = ob + (size_t)b * L;
         uint32_t vlo = (uint32_t)(((uint64_t)nb * part / G) & ~7ull), vhi = part + 1 == G ? nb
                                                                          : (uint32_t)(((uint64_t)nb * (part + 1) / G) & ~7ull);
         if (!terr && !(a.debug & 1)) {
@@ -1614,42 +1652,18 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
             }
           }
         }
-        if (dyn1) {  // the whole block: 16-byte copies when the block is 16-byte aligned
-          __syncwarp();
-          const uint32_t bytes = nb * sh.vb;
-          uint8_t* gd = og + (size_t)b * L * sh.vb;
-          if (!(a.debug & 8)) {
-            if (a.bulk && ((L * sh.vb) & 15) == 0) {
-              const uint32_t n16 = bytes >> 4;
-              uint4* d4 = reinterpret_cast<uint4*>(gd);
-              const uint4* s4 = reinterpret_cast<const uint4*>(ob8);
-              for (uint32_t i = lane; i < n16; i += 32) d4[i] = s4[i];
-              for (uint32_t i = 16 * n16 + lane; i < bytes; i += 32) gd[i] = ob8[i];
-            } else {
-              for (uint32_t i = lane; i < bytes; i += 32) gd[i] = ob8[i];
-            }
-          }
-          __syncwarp();
-          continue;
-        }
-        // store this part's range [vlo, vhi) of block b: bulk interior, plain edges
-        const uint32_t lo = (b * L + vlo) * sh.vb, hi = (b * L + vhi) * sh.vb;
-        if (bst) fence_proxy_async_smem();
-        __syncwarp();
-        const uint32_t a0 = min(hi, (lo + 15) & ~15u), a1 = max(a0, hi & ~15u);
-        if (bst && a1 > a0) {
-          if (lane == 0 && !(a.debug & 8)) bulk_s2g(og + a0, ob8 + a0, a1 - a0);
-          for (uint32_t j = lo + lane; j < a0; j += 32) og[j] = ob8[j];
-          for (uint32_t j = a1 + lane; j < hi; j += 32) og[j] = ob8[j];
-        } else {
-          for (uint32_t j = lo + lane; j < hi; j += 32) og[j] = ob8[j];
-        }
       }
+      if (bst) fence_proxy_async_smem();
+      if (warp == 0 && lane == 0) {
+        C.t_og[s2] = og;
+        C.t_bytes[s2] = nv * sh.vb;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&C.tfull[s2]);
     }
     __syncwarp();
     if (lane == 0) {
       if (warp == 0) TRACE(it, 7);
-      if (bst) bulk_commit();  // one bulk group per warp and tile
       // the last warp done with the stage frees its payload ring space (the
       // stages complete in order: every warp finished the previous one)
       if (atomicAdd(&C.done_cnt[s], 1u) == NCW - 1) {
@@ -1662,7 +1676,6 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       mbar_arrive(&C.empty_in[s]);
     }
   }
-  if (bst && lane == 0) bulk_wait_all<0>();
   err = __reduce_or_sync(0xffffffffu, err);
   if (lane == 0 && err) atomicOr(a.status_out, err);
 }
