@@ -24,6 +24,16 @@
 namespace polyk {
 
 constexpr uint32_t LG_HALO = 64;  // values: >= k_max - 1 (k <= 64)
+// helper-warp waits of the large-block kernels (producer, writer, scheduler,
+// store warp): parked (mbar_wait_helper) or polling
+#ifndef POLY_LARGE_HELPER_PARK
+#define POLY_LARGE_HELPER_PARK 1
+#endif
+#if POLY_LARGE_HELPER_PARK
+#define POLY_LARGE_HWAIT mbar_wait_helper
+#else
+#define POLY_LARGE_HWAIT mbar_wait
+#endif
 
 struct LargeShape {
   uint64_t n, Le, n_blocks;
@@ -126,7 +136,7 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_large(LargeArgs a) {
       const uint32_t nsub = (uint32_t)((nb + sh.SV - 1) / sh.SV);
       const uint8_t* base = a.in + b * sh.Le * sh.vb;
       for (uint32_t c = 0; c < nsub; ++c) {
-        mbar_wait(&C.empty_in[s], ph ^ 1u);
+        POLY_LARGE_HWAIT(&C.empty_in[s], ph ^ 1u);
         const uint64_t v0 = (uint64_t)c * sh.SV;
         const uint32_t nv = (uint32_t)min((uint64_t)sh.SV, nb - v0);
         const uint32_t halo = pass ? (uint32_t)min((uint64_t)LG_HALO, nb - v0 - nv) : 0u;
@@ -171,7 +181,7 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_large(LargeArgs a) {
       if (more) issue(b, 0, seq);
       if (prev != TILE_NONE) issue(prev, 1, seq - 1);
       if (!more) {
-        mbar_wait(&C.empty_in[s], ph ^ 1u);
+        POLY_LARGE_HWAIT(&C.empty_in[s], ph ^ 1u);
         if (lane == 0) {
           C.sb[s] = TILE_NONE;
           C.sseq[s] = seq;  // the writer's end marker goes to slot seq & 1
@@ -189,7 +199,7 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_large(LargeArgs a) {
     // ---------------------------------------------------------- writer: look-back per block
     for (uint32_t i = 0;; ++i) {
       const uint32_t bs = i & 1u, ph = (i >> 1) & 1u;
-      mbar_wait(&C.statsready[bs], ph);
+      POLY_LARGE_HWAIT(&C.statsready[bs], ph);
       const uint64_t b = C.blk[bs];
       if (b == TILE_NONE) break;
       const uint64_t W = C.bnw[bs];
@@ -366,7 +376,7 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_large(LargeArgs a) {
     // then frees it: the consumers never wait for one another.
     for (uint32_t i = 0;; ++i) {
       const uint32_t q = i & 1u;
-      mbar_wait(&C.sfull[q], (i >> 1) & 1u);
+      POLY_LARGE_HWAIT(&C.sfull[q], (i >> 1) & 1u);
       const uint32_t bytes = C.st_bytes[q];
       if (bytes == ~0u) break;
       uint8_t* og = C.st_og[q];
@@ -412,7 +422,7 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_large(LargeArgs a) {
       const uint4 h = hn;
       if (b >= sh.n_blocks) {
         if (lane == 0) {
-          mbar_wait(&C.empty_in[s], ph ^ 1u);
+          POLY_LARGE_HWAIT(&C.empty_in[s], ph ^ 1u);
           C.sb[s] = TILE_NONE;
           mbar_arrive(&C.full_in[s]);
         }
@@ -450,7 +460,7 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_large(LargeArgs a) {
       if (lane == 0 && !e && h.x == CODEC_BASIC) dc = dec_const_of((uint64_t)h.z + 1);
       for (uint32_t c = 0; c < nsub; ++c) {
         if (lane == 0) {
-          mbar_wait(&C.empty_in[s], ph ^ 1u);
+          POLY_LARGE_HWAIT(&C.empty_in[s], ph ^ 1u);
           const uint64_t v0 = (uint64_t)c * sh.SV;
           const uint32_t nv = (uint32_t)min((uint64_t)sh.SV, nb - v0);
           uint64_t j0 = 0, j1 = 0;
