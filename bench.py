@@ -70,6 +70,22 @@ def dist_init(args):
     return rank, world, local
 
 
+def reduce_max(vals, world, dev="cpu"):
+    """Max over ranks of each timing (the job's time is its slowest rank's)."""
+    import torch
+    t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.tolist()]
+
+
+def job_gbs(world, in_bytes, steps, total_ms):
+    """Whole-job throughput: every rank processed `in_bytes` per step (weak
+    scaling, no data-path collective), timed by the slowest rank."""
+    return world * in_bytes * steps / (total_ms * 1e-3) / 1e9
+
+
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -267,12 +283,9 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     comp_ms = [e[0].elapsed_time(e[1]) for e in evs]
     dec_ms = [e[1].elapsed_time(e[2]) for e in evs]
-    t = torch.tensor([total_ms, sum(comp_ms), sum(dec_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, comp_tot, dec_tot = (float(v) for v in t.tolist())
+    total_ms, comp_tot, dec_tot = reduce_max([total_ms, sum(comp_ms), sum(dec_ms)], world, dev)
     K = args.steps
-    value = world * in_bytes * K / (total_ms * 1e-3) / 1e9
+    value = job_gbs(world, in_bytes, K, total_ms)
     comp_avg, dec_avg = comp_tot / K, dec_tot / K
     algo = in_bytes + int_nbytes          # bytes read + written, both kernels
     hbm, peak_src, _ = measured_peaks()
