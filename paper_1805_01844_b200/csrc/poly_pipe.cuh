@@ -177,6 +177,9 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t tx) {
 #define POLY_SUSPEND_NS 0x989680u
 #endif
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity);
+#ifndef POLY_MAP0_BULK_OUT
+#define POLY_MAP0_BULK_OUT 0  // decompress map 0: each group leaves staging by one TMA bulk store (measured slower than the copy)
+#endif
 #ifndef POLY_MAP1_CLAIM
 #define POLY_MAP1_CLAIM 0  // decompress map 1 with G = 1: blocks claimed from a counter (measured slower)
 #endif
@@ -1588,12 +1591,30 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
         const uint4 h = b < nblk ? H[b] : make_uint4(0, 0, 0, 0);
         uint32_t tot;
         const uint32_t ex = warp_excl_scan(min(h.w, 0xfffffu), &tot);
+#if POLY_MAP0_BULK_OUT
+        if (bst) {  // the staging buffer's previous bulk store has read it
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+        }
+#endif
         if (b < nblk && !terr && !(a.debug & 1))
           err |= decode_block0<V>(h, PAY + OFF[g] + ex, min(L, nv - b * L), L, sh.width, bc, ob + (size_t)lane * L);
         __syncwarp();
         const uint32_t bytes = min(nv * sh.vb - g0 * L * sh.vb, gb);
         uint8_t* dst = og + (size_t)g0 * L * sh.vb;
         if (!(a.debug & 8)) {
+#if POLY_MAP0_BULK_OUT
+          if (bst) {  // one bulk store (TMA) of the group; waited for before the buffer is rewritten
+            fence_proxy_async_smem();
+            __syncwarp();
+            const uint32_t b16 = bytes & ~15u;
+            if (lane == 0 && b16) {
+              bulk_s2g(dst, ob8, b16);
+              bulk_commit();
+            }
+            for (uint32_t i = b16 + lane; i < bytes; i += 32) dst[i] = ob8[i];
+          } else
+#endif
           if (a.bulk) {
             // 16-byte copies, lane-strided (a group is at most 4 KiB: <= 8 per lane)
             const uint32_t n16 = bytes >> 4;
@@ -1697,6 +1718,9 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       mbar_arrive(&C.empty_in[s]);
     }
   }
+#if POLY_MAP0_BULK_OUT
+  if (MAP == 0 && bst && lane == 0) bulk_wait_all<0>();  // staging stays valid until the stores read it
+#endif
   err = __reduce_or_sync(0xffffffffu, err);
   if (lane == 0 && err) atomicOr(a.status_out, err);
 }
