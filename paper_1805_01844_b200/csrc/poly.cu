@@ -234,12 +234,16 @@ bool plan_pipe_n(const Shape& sh, PipeShape& ps, bool decomp, uint32_t ncw) {
     ps.o_ring = base + ps.S * stage;
     ps.ring_bytes = (PIPE_SMEM_MAX - ps.o_ring) / 16 * 16;
     if (ps.map == 0 && ps.bpt == 1 && POLY_CMP_WARP_RINGS) {
-      // one word ring per consumer warp, each >= 2 worst-case warp segments
+      // one word ring per consumer warp, each >= 2 worst-case warp segments;
+      // when they do not fit (u32 blocks of many values), the shared ring
       const uint32_t wseg = r16(8ull * 32 * ((sh.Le + kmin - 1) / kmin) + 16);
-      ps.ring_bytes = (PIPE_SMEM_MAX - ps.o_ring) / ncw / 16 * 16;
-      if (ps.ring_bytes < 2 * wseg) return false;
+      const uint32_t per = (PIPE_SMEM_MAX - ps.o_ring) / ncw / 16 * 16;
+      if (per >= 2 * wseg) {
+        ps.wrings = 1;
+        ps.ring_bytes = per;
+      }
     }
-    ps.smem = ps.o_ring + (ps.map == 0 && ps.bpt == 1 && POLY_CMP_WARP_RINGS ? ncw * ps.ring_bytes : ps.ring_bytes);
+    ps.smem = ps.o_ring + (ps.wrings ? ncw * ps.ring_bytes : ps.ring_bytes);
   } else {
     ps.o_off = 16 * ps.TB;
     const uint32_t stage = ps.o_off + r16(4ull * ps.TB);
@@ -530,7 +534,7 @@ poly_status_t poly_compress(const void* d_in, uint64_t n, poly_dtype_t dt, uint6
     pa.debug = debug_flags();
     // per-warp word rings (map 0, one block per thread) move the tile assembly
     // to the writers: 4 of them keep up (measured: 2 -> 1254, 4 -> 2078 GB/s cfg2)
-    const bool wr = pa.sh.map == 0 && pa.sh.bpt == 1 && POLY_CMP_WARP_RINGS;
+    const bool wr = pa.sh.wrings != 0;
     pa.nlb = lb_warps(wr ? 4 : 2, NLB_MAX + 1);
     auto k = dt == POLY_U16 ? (pa.sh.map == 0 ? poly_compress_pipe<uint16_t, 0, NCW_C> : poly_compress_pipe<uint16_t, 1, NCW_C>)
                             : (pa.sh.map == 0 ? poly_compress_pipe<uint32_t, 0, NCW_C> : poly_compress_pipe<uint32_t, 1, NCW_C>);

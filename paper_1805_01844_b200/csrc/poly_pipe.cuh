@@ -93,7 +93,7 @@ struct PipeShape {
   uint32_t o_cache;     // offset of the base-constant cache
   uint32_t o_in, o_out; // offsets of the stages and the staging buffers
   uint32_t o_ring, ring_bytes;  // decompress: payload ring; compress: word slots
-  uint32_t segcap;      // compress: worst-case words of one segment
+  uint32_t wrings;      // compress map 0: per-warp word rings in use (see plan_pipe)
   uint32_t nslot;       // compress: records in flight (<= MAXR)
   uint32_t slot_bytes;  // compress: bytes of each consumer warp's word ring
   uint32_t ncw;         // consumer warps of the kernel instantiation this shape is for
@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
   const uint32_t S = sh.S;
   const BaseCache bc = cache_at(smem + sh.o_cache, false);
   uint8_t* ring = smem + sh.o_ring;
-  const bool WARP_RINGS = MAP == 0 && sh.bpt == 1 && POLY_CMP_WARP_RINGS;  // see plan_pipe
+  const bool WARP_RINGS = MAP == 0 && sh.wrings;  // see plan_pipe
   if (tid == 0) {
     for (uint32_t s = 0; s < S; ++s) {
       mbar_init(&C.full_in[s], 1);

@@ -244,6 +244,7 @@ def _pipe_cases():
         (rng.integers(900, 1100, 4096 * 40).astype(np.uint16), 4096),     # map 1, warp groups per block
         (rng.integers(0, 70000, 7 * 20011).astype(np.uint32), 7),         # map 0, u32, ragged tail
         (rng.integers(0, 5000, 10000 * 260 + 77).astype(np.uint32), 10000),  # large-block regime
+        (rng.integers(0, 1 << 31, 32 * 30011).astype(np.uint32), 32),      # map 0 u32, shared word ring
     ]
 
 
