@@ -416,6 +416,60 @@ int pipe_grid_server(K kernel, int threads, uint32_t smem, uint64_t tiles, int d
 
 }  // namespace
 
+// One poly_compress_pipe launch over tiles [t_begin, t_end) (clipped to the
+// plan); the caller zeroes the status words once per stream and the ticket
+// word before every launch.
+void launch_compress_pipe(const Shape& sh, poly_dtype_t dt, const void* d_in, uint8_t* d_out,
+                          uint64_t* d_compressed_bytes, uint8_t* ws, const WsLayout& W, uint64_t t_begin,
+                          uint64_t t_end, cudaStream_t s, int dev) {
+  PipeArgs pa;
+  memset(&pa, 0, sizeof pa);
+  plan_pipe(sh, pa.sh, false);
+  pa.in = reinterpret_cast<const uint8_t*>(d_in);
+  pa.out = d_out;
+  pa.compressed_bytes = d_compressed_bytes;
+  pa.status = reinterpret_cast<uint64_t*>(ws + W.status_off);
+  pa.ticket = reinterpret_cast<uint32_t*>(ws);
+  pa.bulk = ((reinterpret_cast<uintptr_t>(d_in) & 15) == 0 && pa.sh.tile_bytes % 16 == 0) ? 1u : 0u;
+  pa.debug = debug_flags();
+  pa.t_begin = t_begin;
+  pa.t_end = std::min<uint64_t>(t_end, pa.sh.n_tiles);
+  // per-warp word rings (map 0, one block per thread) move the tile assembly
+  // to the writers: 4 of them keep up (measured: 2 -> 1254, 4 -> 2078 GB/s cfg2)
+  const bool wr = pa.sh.wrings != 0;
+  pa.nlb = lb_warps(wr ? 4 : 2, NLB_MAX + 1);
+  auto k = dt == POLY_U16 ? (pa.sh.map == 0 ? poly_compress_pipe<uint16_t, 0, NCW_C> : poly_compress_pipe<uint16_t, 1, NCW_C>)
+                          : (pa.sh.map == 0 ? poly_compress_pipe<uint32_t, 0, NCW_C> : poly_compress_pipe<uint32_t, 1, NCW_C>);
+  const int grid = pipe_grid_server(k, pipe_threads(NCW_C), pa.sh.smem, pa.t_end - pa.t_begin, dev, pa.server);
+  k<<<grid, pipe_threads(NCW_C), pa.sh.smem, s>>>(pa);
+}
+
+// Streams, events and pinned prefix slots of the chunked host calls.
+constexpr int HOST_CHUNKS = 8;
+struct HostPipe {
+  bool ready = false;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t in[HOST_CHUNKS], kern[HOST_CHUNKS], start;
+  uint64_t* hP = nullptr;  // pinned: inclusive word prefix after each chunk
+};
+HostPipe g_hp[MAX_DEVICES];
+bool host_pipe(int dev, HostPipe*& hp) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  hp = &g_hp[dev];
+  if (hp->ready) return true;
+  if (cudaStreamCreateWithFlags(&hp->h2d, cudaStreamNonBlocking) != cudaSuccess) return false;
+  if (cudaStreamCreateWithFlags(&hp->d2h, cudaStreamNonBlocking) != cudaSuccess) return false;
+  for (int c = 0; c < HOST_CHUNKS; ++c) {
+    if (cudaEventCreateWithFlags(&hp->in[c], cudaEventDisableTiming) != cudaSuccess) return false;
+    if (cudaEventCreateWithFlags(&hp->kern[c], cudaEventDisableTiming) != cudaSuccess) return false;
+  }
+  if (cudaEventCreateWithFlags(&hp->start, cudaEventDisableTiming) != cudaSuccess) return false;
+  if (cudaHostAlloc(reinterpret_cast<void**>(&hp->hP), 8 * HOST_CHUNKS, cudaHostAllocDefault) != cudaSuccess)
+    return false;
+  hp->ready = true;
+  return true;
+}
+
 extern "C" {
 
 int poly_version(void) { return 100; }
@@ -522,24 +576,7 @@ poly_status_t poly_compress(const void* d_in, uint64_t n, poly_dtype_t dt, uint6
     k<<<grid, PT, la.sh.smem, s>>>(la);
   } else if (rg == PIPE) {
     cudaMemsetAsync(ws, 0, W.total, s);
-    PipeArgs pa;
-    memset(&pa, 0, sizeof pa);
-    plan_pipe(sh, pa.sh, false);
-    pa.in = reinterpret_cast<const uint8_t*>(d_in);
-    pa.out = a.out;
-    pa.compressed_bytes = d_compressed_bytes;
-    pa.status = a.status;
-    pa.ticket = a.ticket;
-    pa.bulk = ((reinterpret_cast<uintptr_t>(d_in) & 15) == 0 && pa.sh.tile_bytes % 16 == 0) ? 1u : 0u;
-    pa.debug = debug_flags();
-    // per-warp word rings (map 0, one block per thread) move the tile assembly
-    // to the writers: 4 of them keep up (measured: 2 -> 1254, 4 -> 2078 GB/s cfg2)
-    const bool wr = pa.sh.wrings != 0;
-    pa.nlb = lb_warps(wr ? 4 : 2, NLB_MAX + 1);
-    auto k = dt == POLY_U16 ? (pa.sh.map == 0 ? poly_compress_pipe<uint16_t, 0, NCW_C> : poly_compress_pipe<uint16_t, 1, NCW_C>)
-                            : (pa.sh.map == 0 ? poly_compress_pipe<uint32_t, 0, NCW_C> : poly_compress_pipe<uint32_t, 1, NCW_C>);
-    const int grid = pipe_grid_server(k, pipe_threads(NCW_C), pa.sh.smem, pa.sh.n_tiles, dev, pa.server);
-    k<<<grid, pipe_threads(NCW_C), pa.sh.smem, s>>>(pa);
+    launch_compress_pipe(sh, dt, d_in, a.out, d_compressed_bytes, ws, W, 0, ~0ull, s, dev);
   } else {
     a.bmin = reinterpret_cast<uint32_t*>(ws + W.bmin_off);
     a.bmax = reinterpret_cast<uint32_t*>(ws + W.bmax_off);
@@ -677,6 +714,78 @@ poly_status_t poly_compress_host(const void* h_in, uint64_t n, poly_dtype_t dt, 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   uint8_t* ws = reinterpret_cast<uint8_t*>(d_workspace);
   if (!ws) return POLY_ERR_INVALID_ARG;
+  {
+    // Chunked path (pipeline regime): the values go up in HOST_CHUNKS pieces
+    // on one copy stream, each piece is compressed by a launch over its tiles
+    // (the prefix continues across launches), and each piece's headers and
+    // payload come down on another copy stream while the next piece goes up
+    // -- PCIe carries both directions at once.
+    Shape sh;
+    Regime rg;
+    const uint32_t vb = (uint32_t)dt / 8;
+    if (!getenv("POLY_HOST_SERIAL") && plan(n, (uint32_t)dt, block_size, sh, rg) && rg == PIPE &&
+        (reinterpret_cast<uintptr_t>(d_in_scratch) % 16) == 0 && (reinterpret_cast<uintptr_t>(d_out_scratch) & 15) == 0 &&
+        d_out_capacity >= poly_max_compressed_bytes(n, dt, block_size)) {
+      PipeShape ps;
+      plan_pipe(sh, ps, false);
+      const WsLayout W = ws_layout(sh, rg);
+      const int dev = current_device();
+      HostPipe* hp = nullptr;
+      if (ps.n_tiles >= 2 * HOST_CHUNKS && workspace_bytes >= W.total && ensure_init(dev) == POLY_OK &&
+          host_pipe(dev, hp)) {
+        const uint64_t T = ps.n_tiles, tvals = (uint64_t)ps.TB * sh.Le;
+        const uint8_t* hin = reinterpret_cast<const uint8_t*>(h_in);
+        uint8_t* din = reinterpret_cast<uint8_t*>(d_in_scratch);
+        uint8_t* dout = reinterpret_cast<uint8_t*>(d_out_scratch);
+        uint8_t* hout = reinterpret_cast<uint8_t*>(h_out);
+        uint64_t* d_nbytes = reinterpret_cast<uint64_t*>(ws + 8);
+        const uint64_t* status = reinterpret_cast<const uint64_t*>(ws + W.status_off);
+        uint64_t tb[HOST_CHUNKS + 1];
+        for (int c = 0; c <= HOST_CHUNKS; ++c) tb[c] = T * c / HOST_CHUNKS;
+        // the copy streams start after the caller's earlier work on `s`
+        bool ok = cudaEventRecord(hp->start, s) == cudaSuccess && cudaStreamWaitEvent(hp->h2d, hp->start, 0) == cudaSuccess &&
+                  cudaStreamWaitEvent(hp->d2h, hp->start, 0) == cudaSuccess && cudaMemsetAsync(ws, 0, W.total, s) == cudaSuccess;
+        for (int c = 0; c < HOST_CHUNKS && ok; ++c) {  // values up
+          const uint64_t v0 = std::min<uint64_t>(n, tb[c] * tvals), v1 = std::min<uint64_t>(n, tb[c + 1] * tvals);
+          ok = cudaMemcpyAsync(din + v0 * vb, hin + v0 * vb, (v1 - v0) * vb, cudaMemcpyHostToDevice, hp->h2d) ==
+                   cudaSuccess &&
+               cudaEventRecord(hp->in[c], hp->h2d) == cudaSuccess;
+        }
+        for (int c = 0; c < HOST_CHUNKS && ok; ++c) {  // compress each piece
+          ok = cudaStreamWaitEvent(s, hp->in[c], 0) == cudaSuccess && cudaMemsetAsync(ws, 0, 4, s) == cudaSuccess;
+          if (!ok) break;
+          launch_compress_pipe(sh, dt, d_in_scratch, dout, d_nbytes, ws, W, tb[c], tb[c + 1], s, dev);
+          ok = cudaGetLastError() == cudaSuccess &&
+               cudaMemcpyAsync(hp->hP + c, status + tb[c + 1] - 1, 8, cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+               cudaEventRecord(hp->kern[c], s) == cudaSuccess;
+        }
+        const uint64_t hdr0 = 32, pay0 = 32 + 16 * sh.n_blocks;
+        uint64_t P0 = 0;
+        for (int c = 0; c < HOST_CHUNKS && ok; ++c) {  // stream down, piece by piece
+          ok = cudaEventSynchronize(hp->kern[c]) == cudaSuccess;
+          if (!ok) break;
+          const uint64_t P1 = hp->hP[c] & VAL_MASK;
+          const uint64_t b0 = tb[c] * ps.TB, b1 = std::min<uint64_t>(sh.n_blocks, tb[c + 1] * ps.TB);
+          if (pay0 + 8 * P1 > h_out_capacity) {
+            ok = false;
+            cudaStreamSynchronize(hp->d2h);
+            return POLY_ERR_CAPACITY;
+          }
+          ok = cudaStreamWaitEvent(hp->d2h, hp->kern[c], 0) == cudaSuccess &&
+               cudaMemcpyAsync(hout + hdr0 + 16 * b0, dout + hdr0 + 16 * b0, 16 * (b1 - b0), cudaMemcpyDeviceToHost,
+                               hp->d2h) == cudaSuccess &&
+               (P1 == P0 || cudaMemcpyAsync(hout + pay0 + 8 * P0, dout + pay0 + 8 * P0, 8 * (P1 - P0),
+                                            cudaMemcpyDeviceToHost, hp->d2h) == cudaSuccess);
+          P0 = P1;
+        }
+        if (ok) ok = cudaMemcpyAsync(hout, dout, 32, cudaMemcpyDeviceToHost, hp->d2h) == cudaSuccess;
+        if (cudaStreamSynchronize(hp->d2h) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) ok = false;
+        if (!ok) return POLY_ERR_CUDA;
+        *h_compressed_bytes = pay0 + 8 * P0;
+        return POLY_OK;
+      }
+    }
+  }
   if (cudaMemcpyAsync(d_in_scratch, h_in, n * ((uint32_t)dt / 8), cudaMemcpyHostToDevice, s) != cudaSuccess)
     return POLY_ERR_CUDA;
   uint64_t* d_nbytes = reinterpret_cast<uint64_t*>(ws + 8);

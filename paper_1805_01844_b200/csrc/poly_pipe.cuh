@@ -112,6 +112,7 @@ struct PipeArgs {
   uint32_t debug;           // timing experiments only (POLY_DEBUG): 1 skip compute, 2 skip look-back
   uint32_t nlb;             // look-back / writer warps in use
   uint32_t server;          // 1: the last CTA is the prefix server (see prefix_server)
+  uint64_t t_begin, t_end;  // compress: the tiles of this launch (chunked host calls)
   PipeShape sh;
 };
 
@@ -490,9 +491,11 @@ __device__ __forceinline__ void warp_copy(uint8_t* dst, const uint8_t* src, uint
 // per read.  Its SM carries no bulk traffic, so its reads return quickly; a
 // worker then needs one word, status[t - 1], to learn its tile's offset
 // instead of walking back through other tiles.
-__device__ __noinline__ void prefix_server(uint64_t* status, uint64_t n_tiles) {
+__device__ __noinline__ void prefix_server(uint64_t* status, uint64_t n_tiles, uint64_t t_begin = 0) {
+  // tiles [t_begin, n_tiles); a range after the first continues from the
+  // inclusive prefix the previous launch's server left in status[t_begin - 1]
   const int lane = threadIdx.x & 31;
-  uint64_t P = 0, f = 0;
+  uint64_t P = t_begin ? (ld_relaxed_u64(status + t_begin - 1) & VAL_MASK) : 0, f = t_begin;
   uint32_t ns = 0;
   while (f < n_tiles) {
     uint64_t e[LB_PER];
@@ -562,7 +565,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
   (void)W_LBX;
   extern __shared__ __align__(128) uint8_t smem[];
   if (a.server && blockIdx.x == gridDim.x - 1) {
-    if (threadIdx.x < 32) prefix_server(a.status, a.sh.n_tiles);
+    if (threadIdx.x < 32) prefix_server(a.status, a.t_end, a.t_begin);
     return;
   }
   PipeCtl& C = *reinterpret_cast<PipeCtl*>(smem);
@@ -603,9 +606,9 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
         TRACE(it, 0);
         TRACE_V(it, 10, t32);
       }
-      const uint64_t t = __shfl_sync(0xffffffffu, t32, 0);
+      const uint64_t t = a.t_begin + __shfl_sync(0xffffffffu, t32, 0);
       uint8_t* dst = smem + sh.o_in + (size_t)s * sh.in_stride;
-      if (t >= sh.n_tiles) {
+      if (t >= a.t_end) {
         if (lane == 0) {
           C.tkt[s] = TILE_NONE;
           mbar_arrive(&C.full_in[s]);

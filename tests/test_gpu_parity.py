@@ -272,3 +272,29 @@ def test_repeat_determinism(oracle_lib):
             assert st == 0
             assert np.array_equal(y.cpu().view(torch.int16 if x.dtype == np.uint16 else torch.int32)
                                   .numpy().view(x.dtype), x)
+
+
+@pytest.mark.parametrize("serial", [False, True])
+def test_host_calls(oracle_lib, serial, monkeypatch):
+    """poly_compress_host / poly_decompress_host (pinned host buffers): the
+    chunked, copy-overlapped compress path and the serial one give the oracle's
+    bytes, and the round trip returns the values."""
+    if serial:
+        monkeypatch.setenv("POLY_HOST_SERIAL", "1")
+    rng = np.random.default_rng(99)
+    for x, L in [(rng.integers(240, 275, 30 * 30000).astype(np.uint16), 30),
+                 (rng.integers(1900, 2100, 1024 * 700 + 5).astype(np.uint16), 1024)]:
+        dt = 16
+        n = x.size
+        h_in = torch.from_numpy(x.view(np.int16).copy()).view(torch.uint16).pin_memory()
+        cap = pc.poly_max_compressed_bytes(n, dt, L)
+        d_in = torch.empty(max(cap, 2 * n), dtype=torch.uint8, device="cuda")
+        d_out = torch.empty(max(cap, 2 * n), dtype=torch.uint8, device="cuda")
+        ws = pc.alloc_workspace(n, dt, L, d_in.device)
+        h_stream = torch.empty(cap, dtype=torch.uint8).pin_memory()
+        nb = pc.poly_compress_host(h_in, L, d_in, d_out, ws, h_stream)
+        assert h_stream[:nb].numpy().tobytes() == oracle_lib.compress(x, L)
+        h_out = torch.empty(n, dtype=torch.uint16).pin_memory()
+        st = pc.poly_decompress_host(h_stream, nb, dt, n, L, d_in, d_out, ws, h_out)
+        assert st == 0
+        assert np.array_equal(h_out.view(torch.int16).numpy().view(np.uint16), x)
