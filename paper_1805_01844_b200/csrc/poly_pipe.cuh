@@ -178,6 +178,9 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t tx) {
 #define POLY_SUSPEND_NS 0x989680u
 #endif
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity);
+#ifndef POLY_MAP0_JCAP
+#define POLY_MAP0_JCAP 0  // decompress map 0: full words per block decoded in-lane before the overflow round (0: all; 2 measured slower)
+#endif
 #ifndef POLY_MAP0_BULK_OUT
 #define POLY_MAP0_BULK_OUT 0  // decompress map 0: each group leaves staging by one TMA bulk store (measured slower than the copy)
 #endif
@@ -1153,7 +1156,7 @@ __device__ __forceinline__ void digits_out2(uint32_t a0, uint32_t a1, uint32_t b
 // s < B^mt is checked as s P < B^k).
 template <typename V>
 __device__ __forceinline__ uint32_t decode_block_ent(const uint64_t* src, uint32_t nw, uint32_t B, uint32_t vmin,
-                                                     const DecEnt& e, V* dst) {
+                                                     const DecEnt& e, V* dst, uint32_t jcap, uint32_t* extra) {
   // the constants live in registers for the whole block (the digit stores
   // would otherwise force the compiler to reload them from shared memory)
   const uint64_t Rl = e.Rl, Rh = e.Rh, Wmax = e.Wmax, P = e.P;
@@ -1161,6 +1164,9 @@ __device__ __forceinline__ uint32_t decode_block_ent(const uint64_t* src, uint32
   const uint32_t k = meta & 0xffu, t = (meta >> 16) & 0xffu, add = ((meta >> 8) & 0xffu) ? 0u : 1u;
   uint32_t err = 0;
   const uint32_t nfull = mt < k ? nw - 1 : nw;
+  // full words past jcap are left to the warp's overflow round (decode_group0)
+  const uint32_t nin = min(nfull, jcap);
+  *extra = nfull - nin;
   V* o = dst + (k - 1);
   uint32_t j = 0;
 #if POLY_PAIR_DECODE
@@ -1177,7 +1183,7 @@ __device__ __forceinline__ uint32_t decode_block_ent(const uint64_t* src, uint32
   }
 #endif
 #pragma unroll 1
-  for (; j < nfull; ++j, o += k) {
+  for (; j < nin; ++j, o += k) {
     const uint64_t s = src[j];
     if (s > Wmax) err = POLY_ST_RESIDUE;
     const uint64_t hi1 = __umul64hi(s, Rl), lo2 = s * Rh, hi2 = __umul64hi(s, Rh), mid = lo2 + hi1;
@@ -1200,14 +1206,18 @@ __device__ __forceinline__ uint32_t decode_block_ent(const uint64_t* src, uint32
 // One block of the lane-per-block map (a8, a9): header validation and decode.
 template <typename V>
 __device__ __forceinline__ uint32_t decode_block0(const uint4 h, const uint64_t* src, uint32_t nb, uint32_t L,
-                                                  uint32_t width, const BaseCache& bc, V* dst) {
+                                                  uint32_t width, const BaseCache& bc, V* dst,
+                                                  uint32_t jcap = 0xffffffffu, uint32_t* extra = nullptr) {
   const uint64_t vmax = (width == 16) ? 0xffffull : 0xffffffffull;
+  uint32_t ex0 = 0;
+  if (!extra) extra = &ex0;
+  *extra = 0;
   if (h.x == CODEC_BASIC && h.z != 0 && (uint64_t)h.y + h.z <= vmax) {
     const uint64_t B = (uint64_t)h.z + 1;
     if (B <= CACHE_B && nb == L) {
       const DecEnt& e = bc.E[B];
       if (h.w != e.nwL) return POLY_ST_NWORDS;
-      return decode_block_ent<V>(src, h.w, (uint32_t)B, h.y, e, dst);
+      return decode_block_ent<V>(src, h.w, (uint32_t)B, h.y, e, dst, jcap, extra);
     }
   }
   // general path: partial last block, large bases, constant blocks, errors
@@ -1600,8 +1610,46 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
           __syncwarp();
         }
 #endif
+#if POLY_MAP0_JCAP
+        // the first JCAP full words of every block per lane; the rest (blocks
+        // of small k: more words) spread over the warp's lanes afterwards, so
+        // one such block no longer holds the whole warp for extra rounds
+        uint32_t xw = 0;
+        if (b < nblk && !terr && !(a.debug & 1))
+          err |= decode_block0<V>(h, PAY + OFF[g] + ex, min(L, nv - b * L), L, sh.width, bc,
+                                  ob + (size_t)lane * L, POLY_MAP0_JCAP, &xw);
+        uint32_t totx;
+        const uint32_t exx = warp_excl_scan(xw, &totx);
+#pragma unroll 1
+        for (uint32_t r0 = 0; r0 < totx; r0 += 32) {
+          const uint32_t q = r0 + lane;
+          int o = 0;  // the last lane whose first overflow word is <= q
+#pragma unroll
+          for (int st = 16; st >= 1; st >>= 1) {
+            const uint32_t v = __shfl_sync(0xffffffffu, exx, o + st);
+            if (v <= q) o += st;
+          }
+          const uint32_t jx = POLY_MAP0_JCAP + q - __shfl_sync(0xffffffffu, exx, o);
+          const uint32_t exo = __shfl_sync(0xffffffffu, ex, o);
+          if (q < totx) {
+            const uint4 ho = H[g0 + o];
+            const uint32_t Bo = ho.z + 1;
+            const DecEnt& eo = bc.E[Bo];
+            const uint32_t meta = eo.meta, k = meta & 0xffu, t = (meta >> 16) & 0xffu;
+            const uint32_t add = ((meta >> 8) & 0xffu) ? 0u : 1u;
+            const uint64_t sw = PAY[OFF[g] + exo + jx];
+            if (sw > eo.Wmax) err |= POLY_ST_RESIDUE;
+            const uint64_t Rl = eo.Rl, Rh = eo.Rh;
+            const uint64_t hi1 = __umul64hi(sw, Rl), lo2 = sw * Rh, hi2 = __umul64hi(sw, Rh), mid = lo2 + hi1;
+            const uint64_t f = ((hi2 + (mid < lo2 ? 1ull : 0ull)) << 32) + (mid >> 32) + add;
+            digits_out<V>((uint32_t)f, (uint32_t)(f >> 32), add, Bo, ho.y, (int)(k - t), (int)t,
+                          ob + (size_t)o * L + jx * k + (k - 1));
+          }
+        }
+#else
         if (b < nblk && !terr && !(a.debug & 1))
           err |= decode_block0<V>(h, PAY + OFF[g] + ex, min(L, nv - b * L), L, sh.width, bc, ob + (size_t)lane * L);
+#endif
         __syncwarp();
         const uint32_t bytes = min(nv * sh.vb - g0 * L * sh.vb, gb);
         uint8_t* dst = og + (size_t)g0 * L * sh.vb;
