@@ -444,6 +444,37 @@ void launch_compress_pipe(const Shape& sh, poly_dtype_t dt, const void* d_in, ui
   k<<<grid, pipe_threads(NCW_C), pa.sh.smem, s>>>(pa);
 }
 
+// One poly_decompress_pipe launch over tiles [t_begin, t_end) (clipped).
+void launch_decompress_pipe(const Shape& sh, poly_dtype_t dt, const uint8_t* d_in, uint64_t compressed_bytes,
+                            void* d_out, uint32_t* d_status, uint8_t* ws, const WsLayout& W, uint64_t t_begin,
+                            uint64_t t_end, cudaStream_t s, int dev) {
+  PipeArgs pa;
+  memset(&pa, 0, sizeof pa);
+  plan_pipe(sh, pa.sh, true);
+  pa.in = d_in;
+  pa.out = reinterpret_cast<uint8_t*>(d_out);
+  pa.in_bytes = compressed_bytes;
+  pa.status_out = d_status;
+  pa.status = reinterpret_cast<uint64_t*>(ws + W.status_off);
+  pa.ticket = reinterpret_cast<uint32_t*>(ws);
+  pa.bulk = ((reinterpret_cast<uintptr_t>(d_out) & 15) == 0 && pa.sh.tile_bytes % 16 == 0) ? 1u : 0u;
+  pa.debug = debug_flags();
+  pa.t_begin = t_begin;
+  pa.t_end = std::min<uint64_t>(t_end, pa.sh.n_tiles);
+  // a look-back warp waits on stage i's barrier only after finishing stage
+  // i - nlb, so nlb <= S keeps every parity wait within one phase
+  // (map 1: the last helper warp is the tile store warp)
+  pa.nlb = lb_warps(2, std::min<uint32_t>(pa.sh.map == 1 ? NLB_MAX - 1 : NLB_MAX, pa.sh.S));
+  auto k = dt == POLY_U16
+               ? (pa.sh.map == 0 ? poly_decompress_pipe<uint16_t, 0, NCW_D0>
+                  : pa.sh.ncw == NCW_D1 ? poly_decompress_pipe<uint16_t, 1, NCW_D1> : poly_decompress_pipe<uint16_t, 1, NCW_D1B>)
+               : (pa.sh.map == 0 ? poly_decompress_pipe<uint32_t, 0, NCW_D0>
+                  : pa.sh.ncw == NCW_D1 ? poly_decompress_pipe<uint32_t, 1, NCW_D1> : poly_decompress_pipe<uint32_t, 1, NCW_D1B>);
+  const int nt = pipe_threads((int)pa.sh.ncw);
+  const int grid = pipe_grid_server(k, nt, pa.sh.smem, pa.t_end - pa.t_begin, dev, pa.server);
+  k<<<grid, nt, pa.sh.smem, s>>>(pa);
+}
+
 // Streams, events and pinned prefix slots of the chunked host calls.
 constexpr int HOST_CHUNKS = 8;
 struct HostPipe {
@@ -667,29 +698,7 @@ poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_
     k<<<grid, PT, la.sh.smem, s>>>(la);
   } else if (rg == PIPE) {
     cudaMemsetAsync(ws, 0, W.total, s);
-    PipeArgs pa;
-    memset(&pa, 0, sizeof pa);
-    plan_pipe(sh, pa.sh, true);
-    pa.in = a.in;
-    pa.out = reinterpret_cast<uint8_t*>(d_out);
-    pa.in_bytes = compressed_bytes;
-    pa.status_out = d_status;
-    pa.status = a.status;
-    pa.ticket = a.ticket;
-    pa.bulk = ((reinterpret_cast<uintptr_t>(d_out) & 15) == 0 && pa.sh.tile_bytes % 16 == 0) ? 1u : 0u;
-    pa.debug = debug_flags();
-    // a look-back warp waits on stage i's barrier only after finishing stage
-    // i - nlb, so nlb <= S keeps every parity wait within one phase
-    // (map 1: the last helper warp is the tile store warp)
-    pa.nlb = lb_warps(2, std::min<uint32_t>(pa.sh.map == 1 ? NLB_MAX - 1 : NLB_MAX, pa.sh.S));
-    auto k = dt == POLY_U16
-                 ? (pa.sh.map == 0 ? poly_decompress_pipe<uint16_t, 0, NCW_D0>
-                    : pa.sh.ncw == NCW_D1 ? poly_decompress_pipe<uint16_t, 1, NCW_D1> : poly_decompress_pipe<uint16_t, 1, NCW_D1B>)
-                 : (pa.sh.map == 0 ? poly_decompress_pipe<uint32_t, 0, NCW_D0>
-                    : pa.sh.ncw == NCW_D1 ? poly_decompress_pipe<uint32_t, 1, NCW_D1> : poly_decompress_pipe<uint32_t, 1, NCW_D1B>);
-    const int nt = pipe_threads((int)pa.sh.ncw);
-    const int grid = pipe_grid_server(k, nt, pa.sh.smem, pa.sh.n_tiles, dev, pa.server);
-    k<<<grid, nt, pa.sh.smem, s>>>(pa);
+    launch_decompress_pipe(sh, dt, a.in, compressed_bytes, d_out, d_status, ws, W, 0, ~0ull, s, dev);
   } else {
     a.woff = reinterpret_cast<uint64_t*>(ws + W.woff_off);
     cudaMemsetAsync(ws, 0, W.bmin_off, s);

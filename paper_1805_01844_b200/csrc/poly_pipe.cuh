@@ -1274,7 +1274,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
   (void)W_LBX;
   extern __shared__ __align__(128) uint8_t smem[];
   if (a.server && blockIdx.x == gridDim.x - 1) {
-    if (threadIdx.x < 32 && check_global_header_p_ok(a)) prefix_server(a.status, a.sh.n_tiles);
+    if (threadIdx.x < 32 && check_global_header_p_ok(a)) prefix_server(a.status, a.t_end, a.t_begin);
     return;
   }
   PipeCtl& C = *reinterpret_cast<PipeCtl*>(smem);
@@ -1319,10 +1319,10 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
     uint32_t nend = 0;  // end markers emitted (one per look-back warp)
     for (uint32_t i = 0, s = 0, ph = 0;; ++i) {
       mbar_wait_helper(&C.empty_in[s], ph ^ 1u);
-      const uint64_t t = nend ? sh.n_tiles : atomicAdd(a.ticket, 1u);
+      const uint64_t t = nend ? a.t_end : a.t_begin + atomicAdd(a.ticket, 1u);
       TRACE(i, 0);
       TRACE_V(i, 10, t);
-      if (t >= sh.n_tiles) {
+      if (t >= a.t_end) {
         C.tkt[s] = TILE_NONE;
         mbar_arrive(&C.hbar[s]);
         if (++nend == a.nlb) break;
