@@ -40,7 +40,7 @@ FALLBACK_HBM_GBS = 6650.0
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=100)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -109,16 +109,19 @@ class ClockSampler:
         self._stop = threading.Event()
         self._th = None
 
+    def _sample(self):
+        try:
+            r = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+            if r.returncode == 0 and r.stdout.strip():
+                self.rows.append([c.strip() for c in r.stdout.strip().split(",")])
+        except Exception:
+            pass
+
     def _run(self):
         while not self._stop.is_set():
-            try:
-                r = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
-                                    "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                if r.returncode == 0 and r.stdout.strip():
-                    self.rows.append([c.strip() for c in r.stdout.strip().split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+            self._sample()
+            self._stop.wait(0.05)
 
     def __enter__(self):
         self._th = threading.Thread(target=self._run, daemon=True)
@@ -129,6 +132,7 @@ class ClockSampler:
         self._stop.set()
         if self._th:
             self._th.join(timeout=10)
+        self._sample()  # one more at the end of the timed region (short regions get >= 2)
 
     def summary(self):
         if not self.rows:
