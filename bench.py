@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import statistics
 import os
 import subprocess
 import sys
@@ -176,8 +177,31 @@ def time_oracle(cfg: int, target_seconds: float, steps: int = 1):
         times.append(time.perf_counter() - t0)
         assert st == 0 and np.array_equal(y, x)
     gbs = x.nbytes / (sum(times) / len(times)) / 1e9
+    # one thread on the first 1/threads of the sample's blocks (same per-thread work)
+    L = c.block_len or x.size
+    n1 = max(L, (x.size // max(1, threads)) // L * L) if c.block_len else x.size
+    x1 = x[:n1]
+    t0 = time.perf_counter()
+    s1 = coracle.compress(x1, c.block_len, threads=1)
+    y1, st1 = coracle.decompress(s1, threads=1)
+    t1 = time.perf_counter() - t0
+    assert st1 == 0 and np.array_equal(y1, x1)
     return {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
-            "sample": sample + "; compress+decompress, all host cores"}, times, x.nbytes
+            "sample": sample + "; compress+decompress, all host cores",
+            "single_thread_value": round(x1.nbytes / t1 / 1e9, 4),
+            "single_thread_sample": "first %d values, 1 thread" % n1,
+            "cpu_model": cpu_model()}, times, x.nbytes
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def run_reference(args, rank, world):
@@ -287,6 +311,11 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     comp_ms = [e[0].elapsed_time(e[1]) for e in evs]
     dec_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    per_call = {k: {"median_ms": round(statistics.median(v), 4), "best_ms": round(min(v), 4)}
+                for k, v in (("compress", comp_ms), ("decompress", dec_ms))}
+    graph = None
+    if flush is not None:  # cfg1 (L2-resident): CUDA-graph steady state of one step
+        graph = graph_steady_state(torch, step, stream, args.steps)
     total_ms, comp_tot, dec_tot = reduce_max([total_ms, sum(comp_ms), sum(dec_ms)], world, dev)
     K = args.steps
     value = job_gbs(world, in_bytes, K, total_ms)
@@ -339,12 +368,41 @@ def run_ours(args, rank, world, local):
                      "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
                      "traffic": traffic, "algorithmic_bytes": algo, "peak_source": peak_src,
                      "other_kernel_frac": round(algo / (min(comp_avg, dec_avg) * 1e-3) / 1e9 / hbm, 4)},
+        "per_call": per_call,
+        "graph_steady_state": graph,
         "clocks": clk.summary(),
         "e2e": e2e,
         "gpu_launches": K * (lp_c + lp_d),
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
+
+
+def graph_steady_state(torch, step, stream, steps):
+    """One compress + decompress captured in a CUDA graph and replayed back to
+    back (no L2 flush): the launch-free steady state of the small config."""
+    try:
+        s = torch.cuda.Stream()
+        s.wait_stream(stream)
+        with torch.cuda.stream(s):
+            step()  # the calls read torch's current stream: warm on the capture stream
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step()
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cur = torch.cuda.current_stream()
+        a.record(cur)
+        for _ in range(max(1, steps)):
+            g.replay()
+        b.record(cur)
+        torch.cuda.synchronize()
+        return {"us_per_step": round(1e3 * a.elapsed_time(b) / max(1, steps), 3), "replays": max(1, steps)}
+    except Exception as e:  # pragma: no cover
+        return {"error": str(e)[:200]}
 
 
 def run_e2e(args, pc, torch, x, n, dt, L, in_bytes, nbytes, dev, world):
