@@ -153,6 +153,8 @@ poly_status_t ensure_init(int dev) {
   set_smem_attr(poly_compress_pipe<uint32_t, 0, NCW_C>, pmax);
   set_smem_attr(poly_compress_pipe<uint32_t, 1, NCW_C>, pmax);
   set_smem_attr(poly_decompress_pipe<uint16_t, 0, NCW_D0>, pmax);
+  set_smem_attr(poly_decompress_pipe<uint16_t, 2, NCW_D0>, pmax);
+  set_smem_attr(poly_decompress_pipe<uint32_t, 2, NCW_D0>, pmax);
   set_smem_attr(poly_decompress_pipe<uint16_t, 1, NCW_D1>, pmax);
   set_smem_attr(poly_decompress_pipe<uint16_t, 1, NCW_D1B>, pmax);
   set_smem_attr(poly_decompress_pipe<uint32_t, 1, NCW_D1B>, pmax);
@@ -182,8 +184,20 @@ constexpr uint32_t PIPE_SMEM_MAX = (POLY_CTAS == 1 ? 227 : 113) * 1024;  // shar
 
 uint32_t r16(uint64_t x) { return (uint32_t)((x + 15) / 16 * 16); }
 
+// Binned map-0 decompress (blocks sorted by k within a tile, poly_pipe.cuh
+// MAP 2): 1 = on, 0 = off (POLY_BIN overrides at run time).  Off: measured
+// slower (cfg2 1594 -> 538 GB/s; the per-tile sort in the look-back warps and
+// the half-size tile starve the pipeline).
+#ifndef POLY_MAP0_BIN
+#define POLY_MAP0_BIN 0
+#endif
+static uint32_t bin_div() {
+  const char* e = getenv("POLY_BIN");
+  return e ? (uint32_t)atoi(e) : (uint32_t)POLY_MAP0_BIN;
+}
+
 // Tile shape and shared-memory layout of the pipeline kernels (poly_pipe.cuh).
-bool plan_pipe_n(const Shape& sh, PipeShape& ps, bool decomp, uint32_t ncw) {
+bool plan_pipe_n(const Shape& sh, PipeShape& ps, bool decomp, uint32_t ncw, bool bin = false) {
   const uint32_t pc = 32 * ncw;
   memset(&ps, 0, sizeof ps);
   ps.ncw = ncw;
@@ -201,6 +215,13 @@ bool plan_pipe_n(const Shape& sh, PipeShape& ps, bool decomp, uint32_t ncw) {
     bpt = std::max<uint64_t>(1, std::min<uint64_t>(BPT_MAX, bpt));
     ps.bpt = (uint32_t)bpt;
     ps.TB = (uint32_t)(pc * bpt);
+    if (decomp && bin) {
+      // binned map 0 (poly_pipe.cuh, MAP 2): a tile-wide staging buffer pair,
+      // so a smaller tile (16 NCW blocks; the sorted slots hold a 12-bit block index)
+      ps.map = 2;
+      ps.bpt = 1;
+      ps.TB = 32u * ((ncw + 1) / 2);  // the sort keeps (NCW + 1) / 2 blocks per lane in registers
+    }
   } else {
     ps.map = 1;
     uint64_t tb = PIPE_TILE_TARGET / bb;
@@ -246,13 +267,14 @@ bool plan_pipe_n(const Shape& sh, PipeShape& ps, bool decomp, uint32_t ncw) {
     ps.smem = ps.o_ring + (ps.wrings ? ncw * ps.ring_bytes : ps.ring_bytes);
   } else {
     ps.o_off = 16 * ps.TB;
-    const uint32_t stage = ps.o_off + r16(4ull * ps.TB);
+    // map 2: + 128 sort bins after the slots (poly_pipe.cuh bin_sort)
+    const uint32_t stage = ps.o_off + r16(4ull * ps.TB) + (ps.map == 2 ? 512u : 0u);
     // staging of the decoded values: map 0, one 32-block group per consumer
-    // warp (copied out right after it is decoded); map 1, two tiles (bulk
-    // stores, the buffer is rewritten two tiles later)
+    // warp (copied out right after it is decoded); maps 1 and 2, two tiles
+    // (bulk stores, the buffer is rewritten two tiles later)
     const bool perwarp = ps.map == 0;
     const uint32_t outb = ps.map == 0 ? r16(32ull * bb) : perwarp ? r16(bb) : r16(ps.tile_bytes);
-    const uint32_t outs = perwarp ? ncw * outb : 2 * outb;
+    const uint32_t outs = perwarp ? ncw * outb : (ps.map == 2 ? POLY_BIN_STAGING : 2) * outb;
     // the payload ring (the remainder) holds at least one worst-case tile
     const uint32_t tile_pay = r16(8ull * (ps.words_cap + 2));
     const int64_t room = (int64_t)PIPE_SMEM_MAX - base - (int64_t)outs - (int64_t)tile_pay;
@@ -277,7 +299,10 @@ bool plan_pipe_n(const Shape& sh, PipeShape& ps, bool decomp, uint32_t ncw) {
 bool plan_pipe(const Shape& sh, PipeShape& ps, bool decomp) {
   const bool map0 = (uint64_t)sh.Le * (sh.width / 8) <= MAP0_MAX_BLOCK;
   if (!decomp) return plan_pipe_n(sh, ps, false, NCW_C);
-  if (map0) return plan_pipe_n(sh, ps, true, NCW_D0);
+  if (map0) {
+    if (bin_div() > 0 && plan_pipe_n(sh, ps, true, NCW_D0, true)) return true;
+    return plan_pipe_n(sh, ps, true, NCW_D0);
+  }
   PipeShape a, b;
   const bool oa = plan_pipe_n(sh, a, true, NCW_D1), ob = plan_pipe_n(sh, b, true, NCW_D1B);
   if (oa && (!ob || a.G <= b.G)) {
@@ -381,7 +406,8 @@ int grid_for(uint64_t work, int dev) {
 
 
 // POLY_DEBUG (timing experiments only; the output is then wrong): bit 0 skips
-// the per-block compute, bit 1 the look-back.
+// the per-block compute, bit 1 the look-back; bit 5 (binned map 0 only) keeps
+// the blocks in their own order (the output stays right).
 uint32_t debug_flags() {
   const char* e = getenv("POLY_DEBUG");
   return e ? (uint32_t)strtoul(e, nullptr, 0) : 0u;
@@ -464,11 +490,13 @@ void launch_decompress_pipe(const Shape& sh, poly_dtype_t dt, const uint8_t* d_i
   // a look-back warp waits on stage i's barrier only after finishing stage
   // i - nlb, so nlb <= S keeps every parity wait within one phase
   // (map 1: the last helper warp is the tile store warp)
-  pa.nlb = lb_warps(2, std::min<uint32_t>(pa.sh.map == 1 ? NLB_MAX - 1 : NLB_MAX, pa.sh.S));
+  pa.nlb = lb_warps(2, std::min<uint32_t>(pa.sh.map != 0 ? NLB_MAX - 1 : NLB_MAX, pa.sh.S));
   auto k = dt == POLY_U16
-               ? (pa.sh.map == 0 ? poly_decompress_pipe<uint16_t, 0, NCW_D0>
+               ? (pa.sh.map == 0   ? poly_decompress_pipe<uint16_t, 0, NCW_D0>
+                  : pa.sh.map == 2 ? poly_decompress_pipe<uint16_t, 2, NCW_D0>
                   : pa.sh.ncw == NCW_D1 ? poly_decompress_pipe<uint16_t, 1, NCW_D1> : poly_decompress_pipe<uint16_t, 1, NCW_D1B>)
-               : (pa.sh.map == 0 ? poly_decompress_pipe<uint32_t, 0, NCW_D0>
+               : (pa.sh.map == 0   ? poly_decompress_pipe<uint32_t, 0, NCW_D0>
+                  : pa.sh.map == 2 ? poly_decompress_pipe<uint32_t, 2, NCW_D0>
                   : pa.sh.ncw == NCW_D1 ? poly_decompress_pipe<uint32_t, 1, NCW_D1> : poly_decompress_pipe<uint32_t, 1, NCW_D1B>);
   const int nt = pipe_threads((int)pa.sh.ncw);
   const int grid = pipe_grid_server(k, nt, pa.sh.smem, pa.t_end - pa.t_begin, dev, pa.server);

@@ -132,9 +132,9 @@ struct __align__(16) PipeCtl {
   uint32_t err[MAXS];       // decompress: tile-level status bits
   uint32_t done_cnt[MAXS];  // decompress: warps done with the stage
   uint32_t gnext[MAXS];     // decompress: next group (map 0) / block (map 1, G = 1) of the stage to claim
-  uint64_t tfull[2], tfree[2];  // decompress map 1: staging tile filled (NCW warps) / read by its bulk store
-  uint8_t* t_og[2];             // decompress map 1: destination of the staging tile
-  uint32_t t_bytes[2];          // decompress map 1: its bytes (~0u: end)
+  uint64_t tfull[4], tfree[4];  // decompress maps 1, 2: staging tile filled (NCW warps) / read by its bulk store
+  uint8_t* t_og[4];             // decompress maps 1, 2: destination of the staging tile
+  uint32_t t_bytes[4];          // decompress maps 1, 2: its bytes (~0u: end)
   uint64_t rec_t[MAXR], rec_W[MAXR], rec_end[MAXR];  // compress: staged tiles
   uint64_t rec_empty[MAXR];
   uint32_t rec_off[MAXR];
@@ -1266,10 +1266,75 @@ __device__ __forceinline__ uint32_t decode_tail(const uint64_t* src, uint32_t j0
   return err;
 }
 
+#ifndef POLY_BIN_STAGING
+#define POLY_BIN_STAGING 4  // map 2: decoded tiles staged for their bulk stores (<= 4)
+#endif
+// Binned map 0 (MAP 2): a counting sort of a tile's blocks by k, so that the
+// 32 lanes of a consumer warp decode blocks with the same word count and digit
+// loops (the order within a bucket is free: a block's output position is its
+// own).  OFF[i] = (in-tile word offset << 12) | block of slot i; bins = 128
+// words of the stage after OFF (plan_pipe_n).  Shared-memory atomics rank
+// the blocks; run by the tile's look-back warp while its payload lands.
+template <int QN>
+__device__ __forceinline__ void bin_sort(const uint4* H, uint32_t* OFF, uint32_t* bins, uint32_t nblk, uint32_t L,
+                                         uint32_t nv, const BaseCache& bc, uint32_t lane) {
+  uint32_t off[QN], kp[(QN + 3) / 4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) bins[32 * j + lane] = 0;
+  __syncwarp();
+  uint32_t Wt = 0;
+#pragma unroll
+  for (int q = 0; q < QN; ++q) {
+    const uint32_t b = 32 * q + lane;
+    uint32_t x = 0, key = 127u;  // 127: no block
+    if (b < nblk) {
+      const uint4 h = H[b];
+      x = min(h.w, 0xfffffu);
+      key = 0u;  // general path
+      if (h.x == CODEC_BASIC && h.z != 0 && h.z < CACHE_B && (b + 1) * L <= nv)
+        key = bc.E[h.z + 1].meta & 0xffu;  // k of a full-length cached base
+      atomicAdd(&bins[key], 1u);
+    }
+    uint32_t v = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    off[q] = Wt + v - x;
+    Wt += __shfl_sync(0xffffffffu, v, 31);
+    if (q % 4 == 0) kp[q / 4] = 0;
+    kp[q / 4] |= key << (8 * (q % 4));
+  }
+  __syncwarp();
+  // exclusive scan of bins 0..63 (k <= 64: bin 64 only for B = 2, L >= 64... kept in range below)
+  uint32_t carry = 0;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const uint32_t c = bins[32 * j + lane];
+    uint32_t v = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    __syncwarp();
+    bins[32 * j + lane] = carry + v - c;
+    carry += __shfl_sync(0xffffffffu, v, 31);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < QN; ++q) {
+    const uint32_t key = (kp[q / 4] >> (8 * (q % 4))) & 0xffu;
+    if (key != 127u) OFF[atomicAdd(&bins[key], 1u)] = (off[q] << 12) | (32u * q + lane);
+  }
+}
+
 template <typename V, int MAP, int NW>
 __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_decompress_pipe(PipeArgs a) {
   constexpr int NCW = NW, PC = NW * 32, PT = PC + 32 * (2 + NLB_MAX);
   constexpr int W_PROD = NCW, W_WRIT = NCW + 1, W_HSUM = NCW + 2, W_LBX = NCW + 3;
+  constexpr uint32_t NTS = MAP == 2 ? POLY_BIN_STAGING : 2;  // staging tiles (maps 1, 2)
   (void)W_HSUM;
   (void)W_LBX;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -1287,12 +1352,12 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
     for (uint32_t s = 0; s < S; ++s) {
       mbar_init(&C.hbar[s], 1);
       mbar_init(&C.aggr[s], 1);
-      mbar_init(&C.full_in[s], 1);
+      mbar_init(&C.full_in[s], MAP == 2 ? 2 : 1);  // map 2: + the look-back warp's sort
       mbar_init(&C.empty_in[s], NCW);
       C.done_cnt[s] = 0;
       C.gnext[s] = 0;
     }
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < NTS; ++q) {
       mbar_init(&C.tfull[q], NCW);
       mbar_init(&C.tfree[q], 1);
     }
@@ -1375,9 +1440,10 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       // consumers reject such a block and the look-back warp such a tile.
       const uint32_t* Hw = reinterpret_cast<const uint32_t*>(H) + 3;
       uint32_t Wt = 0;
-      if (MAP == 0) {
+      if (MAP == 0 || MAP == 2) {
         // map 0: only each 32-block group's offset (OFF[g]); a consumer warp
-        // scans within its group.  One warp reduction per group.
+        // scans within its group.  One warp reduction per group.  (Map 2: the
+        // tile's sum only; its look-back warp rewrites OFF with sorted slots.)
         for (uint32_t r0 = 0; r0 < nblk; r0 += 256) {
           uint32_t x[8];
 #pragma unroll
@@ -1445,6 +1511,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       const uint64_t t = C.tkt[s];
       if (t == TILE_NONE) {
         if (lane == 0) mbar_arrive(&C.full_in[s]);
+        if (MAP == 2 && lane == 0) mbar_arrive(&C.full_in[s]);
         break;
       }
       if (lane == 0) TRACE(i, 3);
@@ -1513,16 +1580,42 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
         }
       }
       __syncwarp();
+      if (MAP == 2) {  // the tile's sorted slots, while its payload lands
+        const uint8_t* st = smem + sh.o_in + (size_t)s * sh.in_stride;
+        const uint64_t b0 = t * sh.TB;
+        const uint32_t nblk = (uint32_t)min((uint64_t)sh.TB, sh.n_blocks - b0);
+        const uint32_t nv = (uint32_t)(min(sh.n, b0 * sh.Le + (uint64_t)sh.TB * sh.Le) - b0 * sh.Le);
+        uint32_t* OFFw = reinterpret_cast<uint32_t*>(smem + sh.o_in + (size_t)s * sh.in_stride + sh.o_off);
+        if (a.debug & 32) {  // timing experiment: identity order (valid, unsorted)
+          uint32_t Wt = 0;
+          for (uint32_t r0 = 0; r0 < nblk; r0 += 32) {
+            const uint32_t b = r0 + lane;
+            const uint32_t x = b < nblk ? min(reinterpret_cast<const uint4*>(st)[b].w, 0xfffffu) : 0u;
+            uint32_t v = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+              if (lane >= o) v += y;
+            }
+            if (b < nblk) OFFw[b] = ((Wt + v - x) << 12) | b;
+            Wt += __shfl_sync(0xffffffffu, v, 31);
+          }
+        } else {
+          bin_sort<(NW + 1) / 2>(reinterpret_cast<const uint4*>(st), OFFw, OFFw + sh.TB, nblk, (uint32_t)sh.Le, nv, bc, lane);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&C.full_in[s]);
+      }
     }
     return;
   }
-  if (MAP == 1 && warp == NCW + 1 + NLB_MAX) {
+  if (MAP != 0 && warp == NCW + 1 + NLB_MAX) {
     // ---------------------------------------------------------- tile store warp (map 1)
     // One bulk store per decoded tile, issued once every consumer warp has
     // filled its parts; the staging tile is freed when the store has read it.
     for (uint32_t i = 0;; ++i) {
-      const uint32_t q = i & 1u;
-      mbar_wait_helper(&C.tfull[q], (i >> 1) & 1u);
+      const uint32_t q = i % NTS;
+      mbar_wait_helper(&C.tfull[q], (i / NTS) & 1u);
       const uint32_t bytes = C.t_bytes[q];
       if (bytes == ~0u) break;
       uint8_t* og = C.t_og[q];
@@ -1556,14 +1649,14 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
   const uint32_t L = (uint32_t)sh.Le;
   uint32_t err = 0;
   const bool bst = a.bulk && !(a.debug & 4);
-  for (uint32_t s = 0, ph = 0, s2 = 0, it = 0;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0), s2 ^= 1u, ++it) {
+  for (uint32_t s = 0, ph = 0, s2 = 0, it = 0;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0), s2 = (s2 + 1 == NTS) ? 0 : s2 + 1, ++it) {
     mbar_wait(&C.full_in[s], ph);
     if (lane == 0 && warp == 0) TRACE(it, 6);
     if (lane == 0 && warp == NCW - 1) TRACE(it, 9);
     const uint64_t t = C.tkt[s];
     if (t == TILE_NONE) {
-      if (MAP == 1) {  // end marker for the tile store warp
-        mbar_wait(&C.tfree[s2], ((it >> 1) & 1u) ^ 1u);
+      if (MAP != 0) {  // end marker for the tile store warp
+        mbar_wait(&C.tfree[s2], ((it / NTS) & 1u) ^ 1u);
         if (warp == 0 && lane == 0) C.t_bytes[s2] = ~0u;
         __syncwarp();
         if (lane == 0) mbar_arrive(&C.tfull[s2]);
@@ -1681,12 +1774,39 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
         }
         __syncwarp();
       }
+    } else if (MAP == 2) {
+      // binned map 0: groups of 32 sorted slots (blocks of equal k) claimed
+      // dynamically; each lane decodes its block into the tile's staging
+      // buffer at the block's own position; the tile store warp bulk-stores
+      // the tile once every warp is done with it (as map 1).
+      mbar_wait(&C.tfree[s2], ((it / NTS) & 1u) ^ 1u);
+      const uint32_t ngrp = (nblk + 31) / 32;
+#pragma unroll 1
+      for (;;) {
+        uint32_t g = 0;
+        if (lane == 0) g = atomicAdd(&C.gnext[s], 1u);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        if (g >= ngrp) break;
+        const uint32_t i = g * 32 + lane;
+        if (i < nblk && !terr && !(a.debug & 1)) {
+          const uint32_t e = OFF[i];
+          const uint32_t b = e & 0xfffu;
+          err |= decode_block0<V>(H[b], PAY + (e >> 12), min(L, nv - b * L), L, sh.width, bc, ob + (size_t)b * L);
+        }
+      }
+      if (bst) fence_proxy_async_smem();
+      if (warp == 0 && lane == 0) {
+        C.t_og[s2] = og;
+        C.t_bytes[s2] = nv * sh.vb;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&C.tfull[s2]);
     } else {
       // map 1: part p of a block (G parts) decodes one contiguous range of the
       // block's values into the tile's staging buffer; the tile store warp
       // bulk-stores the whole tile once every warp is done, so no warp waits
       // for another (the buffer was freed by the store of two tiles ago).
-      mbar_wait(&C.tfree[s2], ((it >> 1) & 1u) ^ 1u);
+      mbar_wait(&C.tfree[s2], ((it / NTS) & 1u) ^ 1u);
       const bool claim = sh.G == 1 && POLY_MAP1_CLAIM;
       const uint32_t G = sh.G;
 #pragma unroll 1

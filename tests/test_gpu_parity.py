@@ -249,11 +249,13 @@ def _pipe_cases():
 
 
 @pytest.mark.parametrize("env", [{}, {"POLY_SERVER": "0"}, {"POLY_LB": "1"}, {"POLY_LB": "4"},
-                                 {"POLY_SERVER": "0", "POLY_LB": "3"}])
+                                 {"POLY_SERVER": "0", "POLY_LB": "3"}, {"POLY_BIN": "1"},
+                                 {"POLY_BIN": "1", "POLY_DEBUG": "32"}])
 def test_prefix_and_warp_variants(oracle_lib, env, monkeypatch):
-    """The tile-prefix variants (prefix-server CTA or in-worker look-back) and
-    the look-back / writer warp counts, read at each launch, give the same
-    bytes."""
+    """The tile-prefix variants (prefix-server CTA or in-worker look-back),
+    the look-back / writer warp counts and the binned map-0 decoder (blocks
+    sorted by k; POLY_DEBUG=32: its identity order), read at each launch, give
+    the same bytes."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     for x, L in _pipe_cases():
