@@ -197,7 +197,7 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity);
 #define POLY_WAIT_MIN 32  // first sleep (ns) of a barrier poll
 #endif
 #ifndef POLY_WAIT_BACKOFF
-#define POLY_WAIT_BACKOFF 512  // max sleep (ns) between barrier polls; 0: hardware-suspended try_wait
+#define POLY_WAIT_BACKOFF 256  // max sleep (ns) between barrier polls; 0: hardware-suspended try_wait (measured: 256 > 512, 1024)
 #endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #if POLY_WAIT_BACKOFF > 0
@@ -244,6 +244,20 @@ __device__ __forceinline__ void mbar_wait_helper(uint64_t* bar, uint32_t parity)
       "@!p bra WAITH_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity), "r"(1000000u)
       : "memory");
+#else
+  mbar_wait(bar, parity);
+#endif
+}
+// Decompress consumer waits (next stage's payload, a free staging tile):
+// parked like the helpers (measured against the polling wait: cfg5 1829 ->
+// 1898 GB/s, cfg4 1331 -> 1338, cfg2 unchanged; the compress consumers lose
+// with it and keep polling).
+#ifndef POLY_DEC_PARK
+#define POLY_DEC_PARK 1
+#endif
+__device__ __forceinline__ void mbar_wait_dec(uint64_t* bar, uint32_t parity) {
+#if POLY_DEC_PARK
+  mbar_wait_helper(bar, parity);
 #else
   mbar_wait(bar, parity);
 #endif
@@ -1650,13 +1664,13 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
   uint32_t err = 0;
   const bool bst = a.bulk && !(a.debug & 4);
   for (uint32_t s = 0, ph = 0, s2 = 0, it = 0;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0), s2 = (s2 + 1 == NTS) ? 0 : s2 + 1, ++it) {
-    mbar_wait(&C.full_in[s], ph);
+    mbar_wait_dec(&C.full_in[s], ph);
     if (lane == 0 && warp == 0) TRACE(it, 6);
     if (lane == 0 && warp == NCW - 1) TRACE(it, 9);
     const uint64_t t = C.tkt[s];
     if (t == TILE_NONE) {
       if (MAP != 0) {  // end marker for the tile store warp
-        mbar_wait(&C.tfree[s2], ((it / NTS) & 1u) ^ 1u);
+        mbar_wait_dec(&C.tfree[s2], ((it / NTS) & 1u) ^ 1u);
         if (warp == 0 && lane == 0) C.t_bytes[s2] = ~0u;
         __syncwarp();
         if (lane == 0) mbar_arrive(&C.tfull[s2]);
@@ -1779,7 +1793,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       // dynamically; each lane decodes its block into the tile's staging
       // buffer at the block's own position; the tile store warp bulk-stores
       // the tile once every warp is done with it (as map 1).
-      mbar_wait(&C.tfree[s2], ((it / NTS) & 1u) ^ 1u);
+      mbar_wait_dec(&C.tfree[s2], ((it / NTS) & 1u) ^ 1u);
       const uint32_t ngrp = (nblk + 31) / 32;
 #pragma unroll 1
       for (;;) {
@@ -1806,7 +1820,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       // block's values into the tile's staging buffer; the tile store warp
       // bulk-stores the whole tile once every warp is done, so no warp waits
       // for another (the buffer was freed by the store of two tiles ago).
-      mbar_wait(&C.tfree[s2], ((it / NTS) & 1u) ^ 1u);
+      mbar_wait_dec(&C.tfree[s2], ((it / NTS) & 1u) ^ 1u);
       const bool claim = sh.G == 1 && POLY_MAP1_CLAIM;
       const uint32_t G = sh.G;
 #pragma unroll 1
