@@ -34,6 +34,15 @@ constexpr uint32_t LG_HALO = 64;  // values: >= k_max - 1 (k <= 64)
 #else
 #define POLY_LARGE_HWAIT mbar_wait
 #endif
+// large-block consumer waits (input stage, published prefix, free staging)
+#ifndef POLY_LARGE_CONSUMER_PARK
+#define POLY_LARGE_CONSUMER_PARK 1  // measured: cfg3 decompress 1830 -> 1854, compress 2027 -> 2048
+#endif
+#if POLY_LARGE_CONSUMER_PARK
+#define POLY_LARGE_CWAIT mbar_wait_helper
+#else
+#define POLY_LARGE_CWAIT mbar_wait
+#endif
 
 struct LargeShape {
   uint64_t n, Le, n_blocks;
@@ -229,7 +238,7 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_large(LargeArgs a) {
   // ------------------------------------------------------------ consumers
   uint4* hdr_g = reinterpret_cast<uint4*>(a.out + 32);
   for (uint32_t s = 0, ph = 0;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0)) {
-    mbar_wait(&C.full_in[s], ph);
+    POLY_LARGE_CWAIT(&C.full_in[s], ph);
     const uint64_t b = C.sb[s];
     const uint32_t seq = C.sseq[s];
     if (b == TILE_NONE) {
@@ -278,7 +287,7 @@ __global__ void __launch_bounds__(PT, 1) poly_compress_large(LargeArgs a) {
     } else {
       // ---- a5: words whose first value lies in this sub-tile, straight to HBM
       const uint32_t bs = seq & 1u;
-      mbar_wait(&C.prefixready[bs], (seq >> 1) & 1u);
+      POLY_LARGE_CWAIT(&C.prefixready[bs], (seq >> 1) & 1u);
       const uint32_t bm1 = C.bbm1[bs];
       if (bm1 != 0) {
         const uint32_t vmin = C.bvmin[bs], k = C.bk[bs];
@@ -504,10 +513,10 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_large(LargeArgs a) {
   uint32_t err = 0;
   for (uint32_t s = 0, ph = 0, i = 0;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0), ++i) {
     const uint32_t s2 = i & 1u;
-    mbar_wait(&C.full_in[s], ph);
+    POLY_LARGE_CWAIT(&C.full_in[s], ph);
     const uint64_t b = C.sb[s];
     if (b == TILE_NONE) {
-      mbar_wait(&C.sfree[s2], ((i >> 1) & 1u) ^ 1u);
+      POLY_LARGE_CWAIT(&C.sfree[s2], ((i >> 1) & 1u) ^ 1u);
       if (tid == 0) C.st_bytes[s2] = ~0u;  // end marker for the store warp
       __syncwarp();
       if (lane == 0) mbar_arrive(&C.sfull[s2]);
@@ -521,7 +530,7 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_large(LargeArgs a) {
     const uint64_t nb = blk_len(sh, b);
     const uint64_t v0 = (uint64_t)c * sh.SV;
     if (tid == 0 && c == 0) err |= e;
-    mbar_wait(&C.sfree[s2], ((i >> 1) & 1u) ^ 1u);  // the buffer's store of two sub-tiles ago has read it
+    POLY_LARGE_CWAIT(&C.sfree[s2], ((i >> 1) & 1u) ^ 1u);  // the buffer's store of two sub-tiles ago has read it
     if (!e) {
       if (h.x == CODEC_CONSTANT) {
         for (uint32_t i2 = tid; i2 < nv; i2 += PC) ob[i2] = (V)h.y;
