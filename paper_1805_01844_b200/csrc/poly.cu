@@ -191,9 +191,9 @@ uint32_t r16(uint64_t x) { return (uint32_t)((x + 15) / 16 * 16); }
 #ifndef POLY_MAP0_BIN
 #define POLY_MAP0_BIN 0
 #endif
-static uint32_t bin_div() {
+static bool bin_enabled() {
   const char* e = getenv("POLY_BIN");
-  return e ? (uint32_t)atoi(e) : (uint32_t)POLY_MAP0_BIN;
+  return e ? atoi(e) != 0 : POLY_MAP0_BIN != 0;
 }
 
 // Tile shape and shared-memory layout of the pipeline kernels (poly_pipe.cuh).
@@ -300,7 +300,7 @@ bool plan_pipe(const Shape& sh, PipeShape& ps, bool decomp) {
   const bool map0 = (uint64_t)sh.Le * (sh.width / 8) <= MAP0_MAX_BLOCK;
   if (!decomp) return plan_pipe_n(sh, ps, false, NCW_C);
   if (map0) {
-    if (bin_div() > 0 && plan_pipe_n(sh, ps, true, NCW_D0, true)) return true;
+    if (bin_enabled() && plan_pipe_n(sh, ps, true, NCW_D0, true)) return true;
     return plan_pipe_n(sh, ps, true, NCW_D0);
   }
   PipeShape a, b;
