@@ -64,6 +64,14 @@ typedef enum {
 /* Library version (major*10000 + minor*100 + patch). */
 int poly_version(void);
 
+/* Host-only self-check (no device needed): builds the per-base tables with
+ * exact 128-bit integers and returns 1 if every precondition of the decoder
+ * arithmetic holds (B^k < 2^64 - 2^32 for non-powers of
+ * two; the compile-time T32MIN[K] of the k-specialised decoders equals the
+ * least t32 over the non-power-of-two bases of capacity K), else 0.
+ * poly_init fails with POLY_ERR_CUDA in the second case. */
+int poly_tables_ok(void);
+
 /* Human-readable name of a poly_status_t. */
 const char* poly_status_string(poly_status_t s);
 

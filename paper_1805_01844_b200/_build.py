@@ -15,7 +15,7 @@ if VARIANT_FLAGS:
     LIB = os.path.join(HERE, "libpolycomp_%s.so" % os.environ.get("POLY_VARIANT_NAME", "variant"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 SOURCES = ["poly.cu"]
-DEPS = ["poly.cu", "poly_common.cuh", "poly_compress.cuh", "poly_decompress.cuh", "poly_word.cuh", "poly_pipe.cuh", "poly_kword.cuh", "poly_large.cuh"]
+DEPS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh")))
 
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -120,6 +120,23 @@ void build_tables() {
     h_ktab[B] = (uint16_t)(k | (h << 8));
     h_dtab[B] = c;
   }
+  // The k-specialised u16 decoders (poly_kword.cuh) switch to 32-bit steps at
+  // the compile-time T32MIN[K]; it must be the least t32 over the
+  // non-power-of-two bases of capacity K, else poly_init
+  // fails (POLY_ERR_CUDA) rather than decode wrongly.
+  {
+    int lo[65];
+    for (int K = 0; K <= 64; ++K) lo[K] = 1 << 30;
+    for (uint64_t B = 3; B <= KTAB_MAX; ++B) {
+      if ((B & (B - 1)) == 0) continue;
+      const int K = (int)(h_dtab[B].meta & 0xffu), t = (int)((h_dtab[B].meta >> 16) & 0xffu);
+      lo[K] = std::min(lo[K], t);
+    }
+#define POLY_CHECK_T32(KK) \
+  if (lo[KK] != (1 << 30) && lo[KK] != t32min_u16(KK)) h_tables_bad = true; /* K = 21: B = 8 only */
+    POLY_FOR_EACH_K16(POLY_CHECK_T32)
+#undef POLY_CHECK_T32
+  }
   h_tables_built = true;
 }
 
@@ -153,8 +170,6 @@ poly_status_t ensure_init(int dev) {
   set_smem_attr(poly_compress_pipe<uint32_t, 0, NCW_C>, pmax);
   set_smem_attr(poly_compress_pipe<uint32_t, 1, NCW_C>, pmax);
   set_smem_attr(poly_decompress_pipe<uint16_t, 0, NCW_D0>, pmax);
-  set_smem_attr(poly_decompress_pipe<uint16_t, 2, NCW_D0>, pmax);
-  set_smem_attr(poly_decompress_pipe<uint32_t, 2, NCW_D0>, pmax);
   set_smem_attr(poly_decompress_pipe<uint16_t, 1, NCW_D1>, pmax);
   set_smem_attr(poly_decompress_pipe<uint16_t, 1, NCW_D1B>, pmax);
   set_smem_attr(poly_decompress_pipe<uint32_t, 1, NCW_D1B>, pmax);
@@ -184,20 +199,8 @@ constexpr uint32_t PIPE_SMEM_MAX = (POLY_CTAS == 1 ? 227 : 113) * 1024;  // shar
 
 uint32_t r16(uint64_t x) { return (uint32_t)((x + 15) / 16 * 16); }
 
-// Binned map-0 decompress (blocks sorted by k within a tile, poly_pipe.cuh
-// MAP 2): 1 = on, 0 = off (POLY_BIN overrides at run time).  Off: measured
-// slower (cfg2 1594 -> 538 GB/s; the per-tile sort in the look-back warps and
-// the half-size tile starve the pipeline).
-#ifndef POLY_MAP0_BIN
-#define POLY_MAP0_BIN 0
-#endif
-static bool bin_enabled() {
-  const char* e = getenv("POLY_BIN");
-  return e ? atoi(e) != 0 : POLY_MAP0_BIN != 0;
-}
-
 // Tile shape and shared-memory layout of the pipeline kernels (poly_pipe.cuh).
-bool plan_pipe_n(const Shape& sh, PipeShape& ps, bool decomp, uint32_t ncw, bool bin = false) {
+bool plan_pipe_n(const Shape& sh, PipeShape& ps, bool decomp, uint32_t ncw) {
   const uint32_t pc = 32 * ncw;
   memset(&ps, 0, sizeof ps);
   ps.ncw = ncw;
@@ -215,13 +218,6 @@ bool plan_pipe_n(const Shape& sh, PipeShape& ps, bool decomp, uint32_t ncw, bool
     bpt = std::max<uint64_t>(1, std::min<uint64_t>(BPT_MAX, bpt));
     ps.bpt = (uint32_t)bpt;
     ps.TB = (uint32_t)(pc * bpt);
-    if (decomp && bin) {
-      // binned map 0 (poly_pipe.cuh, MAP 2): a tile-wide staging buffer pair,
-      // so a smaller tile (16 NCW blocks; the sorted slots hold a 12-bit block index)
-      ps.map = 2;
-      ps.bpt = 1;
-      ps.TB = 32u * ((ncw + 1) / 2);  // the sort keeps (NCW + 1) / 2 blocks per lane in registers
-    }
   } else {
     ps.map = 1;
     uint64_t tb = PIPE_TILE_TARGET / bb;
@@ -267,14 +263,13 @@ bool plan_pipe_n(const Shape& sh, PipeShape& ps, bool decomp, uint32_t ncw, bool
     ps.smem = ps.o_ring + (ps.wrings ? ncw * ps.ring_bytes : ps.ring_bytes);
   } else {
     ps.o_off = 16 * ps.TB;
-    // map 2: + 128 sort bins after the slots (poly_pipe.cuh bin_sort)
-    const uint32_t stage = ps.o_off + r16(4ull * ps.TB) + (ps.map == 2 ? 512u : 0u);
+    const uint32_t stage = ps.o_off + r16(4ull * ps.TB);
     // staging of the decoded values: map 0, one 32-block group per consumer
-    // warp (copied out right after it is decoded); maps 1 and 2, two tiles
+    // warp (copied out right after it is decoded); map 1, two tiles
     // (bulk stores, the buffer is rewritten two tiles later)
     const bool perwarp = ps.map == 0;
     const uint32_t outb = ps.map == 0 ? r16(32ull * bb) : perwarp ? r16(bb) : r16(ps.tile_bytes);
-    const uint32_t outs = perwarp ? ncw * outb : (ps.map == 2 ? POLY_BIN_STAGING : 2) * outb;
+    const uint32_t outs = perwarp ? ncw * outb : 2 * outb;
     // the payload ring (the remainder) holds at least one worst-case tile
     const uint32_t tile_pay = r16(8ull * (ps.words_cap + 2));
     const int64_t room = (int64_t)PIPE_SMEM_MAX - base - (int64_t)outs - (int64_t)tile_pay;
@@ -299,10 +294,7 @@ bool plan_pipe_n(const Shape& sh, PipeShape& ps, bool decomp, uint32_t ncw, bool
 bool plan_pipe(const Shape& sh, PipeShape& ps, bool decomp) {
   const bool map0 = (uint64_t)sh.Le * (sh.width / 8) <= MAP0_MAX_BLOCK;
   if (!decomp) return plan_pipe_n(sh, ps, false, NCW_C);
-  if (map0) {
-    if (bin_enabled() && plan_pipe_n(sh, ps, true, NCW_D0, true)) return true;
-    return plan_pipe_n(sh, ps, true, NCW_D0);
-  }
+  if (map0) return plan_pipe_n(sh, ps, true, NCW_D0);
   PipeShape a, b;
   const bool oa = plan_pipe_n(sh, a, true, NCW_D1), ob = plan_pipe_n(sh, b, true, NCW_D1B);
   if (oa && (!ob || a.G <= b.G)) {
@@ -355,6 +347,9 @@ bool plan(uint64_t n, uint32_t w, uint64_t block_size, Shape& sh, Regime& rg) {
   sh.Le = block_size == 0 ? n : block_size;
   sh.n_blocks = (n + sh.Le - 1) / sh.Le;
   if (sh.n_blocks >= (1ull << 32)) return false;
+  // a block header holds n_words in 32 bits: ceil(L_e / k_min) < 2^32 (only a
+  // block_size = 0 call with n >= 2^33 (u32) / 2^34 (u16) exceeds it)
+  if ((sh.Le + (w == 16 ? 3 : 1)) / (w == 16 ? 4 : 2) >= (1ull << 32)) return false;
   const uint64_t bb = sh.Le * (w / 8);  // bytes per block
   PipeShape pc, pd;
   LargeShape lc, ld;
@@ -405,19 +400,19 @@ int grid_for(uint64_t work, int dev) {
 }
 
 
-// POLY_DEBUG (timing experiments only; the output is then wrong): bit 0 skips
-// the per-block compute, bit 1 the look-back; bit 5 (binned map 0 only) keeps
-// the blocks in their own order (the output stays right).
+#ifdef POLY_TIMING
+// Timing-experiment variant library only (never the product library): the
+// POLY_DEBUG bits skip per-block compute (1), the look-back (2) or stores
+// (4, 8, 16); the output is then wrong (profiles/ab_bench.sh).
 uint32_t debug_flags() {
   const char* e = getenv("POLY_DEBUG");
   return e ? (uint32_t)strtoul(e, nullptr, 0) : 0u;
 }
-// Look-back warps per CTA (1 or 2); POLY_LB overrides the default.
-uint32_t lb_warps(uint32_t dflt, uint32_t vmax) {
-  const char* e = getenv("POLY_LB");
-  const uint32_t v = e ? (uint32_t)strtoul(e, nullptr, 0) : dflt;
-  return std::max(1u, std::min(v, vmax));
-}
+#else
+uint32_t debug_flags() { return 0u; }
+#endif
+// Look-back / writer warps per CTA.
+uint32_t lb_warps(uint32_t dflt, uint32_t vmax) { return std::max(1u, std::min(dflt, vmax)); }
 
 template <typename K>
 int pipe_grid(K kernel, uint32_t smem, uint64_t tiles, int dev, int threads = PT) {
@@ -428,16 +423,35 @@ int pipe_grid(K kernel, uint32_t smem, uint64_t tiles, int dev, int threads = PT
   return (int)std::max<uint64_t>(1, std::min<uint64_t>(cap, tiles));
 }
 // Grid of a pipeline launch: worker CTAs plus, when there is more than one
-// tile, the prefix-server CTA (all resident: the grid never exceeds what fits).
-// POLY_SERVER=0 selects the in-worker decoupled look-back instead.
+// tile, the prefix-server CTA.  Every worker of tile t >= 1 waits on the
+// server, so the grid must be co-resident: such launches are cooperative
+// (launch_k), which the driver only starts when every CTA fits (it never
+// exceeds the occupancy bound computed here).
 template <typename K>
 int pipe_grid_server(K kernel, int threads, uint32_t smem, uint64_t tiles, int dev, uint32_t& server) {
-  const char* e = getenv("POLY_SERVER");
-  const bool want = !(e && e[0] == '0');
   const int cap = pipe_grid(kernel, smem, ~0ull, dev, threads);
-  server = (want && tiles > 1 && cap >= 2) ? 1u : 0u;
+  server = (tiles > 1 && cap >= 2) ? 1u : 0u;
   const uint64_t workers = std::min<uint64_t>(tiles, (uint64_t)cap - server);
   return (int)(std::max<uint64_t>(1, workers) + server);
+}
+
+// Launch `kernel` (cooperatively when `coop`: a grid whose CTAs wait on one
+// another -- the prefix server -- must be resident all at once).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kernel)(KArgs...), int grid, int threads, uint32_t smem, cudaStream_t s, bool coop,
+                     Args... args) {
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof cfg);
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = coop ? attr : nullptr;
+  cfg.numAttrs = coop ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
 }  // namespace
@@ -467,7 +481,7 @@ void launch_compress_pipe(const Shape& sh, poly_dtype_t dt, const void* d_in, ui
   auto k = dt == POLY_U16 ? (pa.sh.map == 0 ? poly_compress_pipe<uint16_t, 0, NCW_C> : poly_compress_pipe<uint16_t, 1, NCW_C>)
                           : (pa.sh.map == 0 ? poly_compress_pipe<uint32_t, 0, NCW_C> : poly_compress_pipe<uint32_t, 1, NCW_C>);
   const int grid = pipe_grid_server(k, pipe_threads(NCW_C), pa.sh.smem, pa.t_end - pa.t_begin, dev, pa.server);
-  k<<<grid, pipe_threads(NCW_C), pa.sh.smem, s>>>(pa);
+  launch_k(k, grid, pipe_threads(NCW_C), pa.sh.smem, s, pa.server != 0, pa);
 }
 
 // One poly_decompress_pipe launch over tiles [t_begin, t_end) (clipped).
@@ -494,14 +508,12 @@ void launch_decompress_pipe(const Shape& sh, poly_dtype_t dt, const uint8_t* d_i
   pa.nlb = lb_warps(pa.sh.map == 1 ? 1 : 2, std::min<uint32_t>(pa.sh.map != 0 ? NLB_MAX - 1 : NLB_MAX, pa.sh.S));
   auto k = dt == POLY_U16
                ? (pa.sh.map == 0   ? poly_decompress_pipe<uint16_t, 0, NCW_D0>
-                  : pa.sh.map == 2 ? poly_decompress_pipe<uint16_t, 2, NCW_D0>
                   : pa.sh.ncw == NCW_D1 ? poly_decompress_pipe<uint16_t, 1, NCW_D1> : poly_decompress_pipe<uint16_t, 1, NCW_D1B>)
                : (pa.sh.map == 0   ? poly_decompress_pipe<uint32_t, 0, NCW_D0>
-                  : pa.sh.map == 2 ? poly_decompress_pipe<uint32_t, 2, NCW_D0>
                   : pa.sh.ncw == NCW_D1 ? poly_decompress_pipe<uint32_t, 1, NCW_D1> : poly_decompress_pipe<uint32_t, 1, NCW_D1B>);
   const int nt = pipe_threads((int)pa.sh.ncw);
   const int grid = pipe_grid_server(k, nt, pa.sh.smem, pa.t_end - pa.t_begin, dev, pa.server);
-  k<<<grid, nt, pa.sh.smem, s>>>(pa);
+  launch_k(k, grid, nt, pa.sh.smem, s, pa.server != 0, pa);
 }
 
 // Streams, events and pinned prefix slots of the chunked host calls.
@@ -513,6 +525,9 @@ struct HostPipe {
   uint64_t* hP = nullptr;  // pinned: inclusive word prefix after each chunk
 };
 HostPipe g_hp[MAX_DEVICES];
+// One chunked host call per device at a time: the events and the pinned
+// prefix slots of g_hp[dev] are per device, not per call.
+std::mutex g_host_mu[MAX_DEVICES];
 bool host_pipe(int dev, HostPipe*& hp) {
   std::lock_guard<std::mutex> lk(g_mu);
   hp = &g_hp[dev];
@@ -532,7 +547,13 @@ bool host_pipe(int dev, HostPipe*& hp) {
 
 extern "C" {
 
-int poly_version(void) { return 100; }
+int poly_version(void) { return 200; }
+
+int poly_tables_ok(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  build_tables();
+  return h_tables_bad ? 0 : 1;
+}
 
 const char* poly_status_string(poly_status_t s) {
   switch (s) {
@@ -633,7 +654,7 @@ poly_status_t poly_compress(const void* d_in, uint64_t n, poly_dtype_t dt, uint6
     la.bulk = ((reinterpret_cast<uintptr_t>(d_in) & 15) == 0 && (sh.Le * (dt / 8)) % 16 == 0) ? 1u : 0u;
     auto k = dt == POLY_U16 ? poly_compress_large<uint16_t> : poly_compress_large<uint32_t>;
     const int grid = pipe_grid_server(k, PT, la.sh.smem, sh.n_blocks, dev, la.server);
-    k<<<grid, PT, la.sh.smem, s>>>(la);
+    launch_k(k, grid, PT, la.sh.smem, s, la.server != 0, la);
   } else if (rg == PIPE) {
     cudaMemsetAsync(ws, 0, W.total, s);
     launch_compress_pipe(sh, dt, d_in, a.out, d_compressed_bytes, ws, W, 0, ~0ull, s, dev);
@@ -724,7 +745,7 @@ poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_
     la.bulk = ((reinterpret_cast<uintptr_t>(d_out) & 15) == 0 && (sh.Le * (dt / 8)) % 16 == 0) ? 1u : 0u;
     auto k = dt == POLY_U16 ? poly_decompress_large<uint16_t> : poly_decompress_large<uint32_t>;
     const int grid = pipe_grid_server(k, PT, la.sh.smem, sh.n_blocks, dev, la.server);
-    k<<<grid, PT, la.sh.smem, s>>>(la);
+    launch_k(k, grid, PT, la.sh.smem, s, la.server != 0, la);
   } else if (rg == PIPE) {
     cudaMemsetAsync(ws, 0, W.total, s);
     launch_decompress_pipe(sh, dt, a.in, compressed_bytes, d_out, d_status, ws, W, 0, ~0ull, s, dev);
@@ -761,7 +782,7 @@ poly_status_t poly_compress_host(const void* h_in, uint64_t n, poly_dtype_t dt, 
     Shape sh;
     Regime rg;
     const uint32_t vb = (uint32_t)dt / 8;
-    if (!getenv("POLY_HOST_SERIAL") && plan(n, (uint32_t)dt, block_size, sh, rg) && rg == PIPE &&
+    if (plan(n, (uint32_t)dt, block_size, sh, rg) && rg == PIPE &&
         (reinterpret_cast<uintptr_t>(d_in_scratch) % 16) == 0 && (reinterpret_cast<uintptr_t>(d_out_scratch) & 15) == 0 &&
         d_out_capacity >= poly_max_compressed_bytes(n, dt, block_size)) {
       PipeShape ps;
@@ -771,6 +792,7 @@ poly_status_t poly_compress_host(const void* h_in, uint64_t n, poly_dtype_t dt, 
       HostPipe* hp = nullptr;
       if (ps.n_tiles >= 2 * HOST_CHUNKS && workspace_bytes >= W.total && ensure_init(dev) == POLY_OK &&
           host_pipe(dev, hp)) {
+        std::lock_guard<std::mutex> call_lock(g_host_mu[dev]);
         const uint64_t T = ps.n_tiles, tvals = (uint64_t)ps.TB * sh.Le;
         const uint8_t* hin = reinterpret_cast<const uint8_t*>(h_in);
         uint8_t* din = reinterpret_cast<uint8_t*>(d_in_scratch);
@@ -805,7 +827,9 @@ poly_status_t poly_compress_host(const void* h_in, uint64_t n, poly_dtype_t dt, 
           const uint64_t P1 = hp->hP[c] & VAL_MASK;
           const uint64_t b0 = tb[c] * ps.TB, b1 = std::min<uint64_t>(sh.n_blocks, tb[c + 1] * ps.TB);
           if (pay0 + 8 * P1 > h_out_capacity) {
-            ok = false;
+            // drain every copy and kernel of this call before returning
+            cudaStreamSynchronize(s);
+            cudaStreamSynchronize(hp->h2d);
             cudaStreamSynchronize(hp->d2h);
             return POLY_ERR_CAPACITY;
           }

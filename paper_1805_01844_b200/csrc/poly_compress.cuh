@@ -7,6 +7,7 @@
 // than 32 KiB, e.g. cfg1's single block); see poly.cu plan().
 #pragma once
 #include "poly_common.cuh"
+#include "poly_word.cuh"
 
 namespace polyk {
 
@@ -21,21 +22,6 @@ struct CompressArgs {
   uint64_t* woff;     // large regime: per-block payload word offset
   Shape sh;
 };
-
-__device__ __forceinline__ void write_global_header(uint8_t* out, const Shape& sh,
-                                                    uint64_t payload_words) {
-  uint4 h0, h1;
-  h0.x = 0x43594c50u;                                   // "PLYC" little-endian
-  h0.y = 2u | (0u << 8) | (sh.width << 16) | (0u << 24);  // version, layout, width, policy
-  h0.z = (uint32_t)sh.n;
-  h0.w = (uint32_t)(sh.n >> 32);
-  h1.x = sh.block_len;
-  h1.y = (uint32_t)sh.n_blocks;
-  h1.z = (uint32_t)(payload_words * 8);
-  h1.w = (uint32_t)((payload_words * 8) >> 32);
-  reinterpret_cast<uint4*>(out)[0] = h0;
-  reinterpret_cast<uint4*>(out)[1] = h1;
-}
 
 // Horner evaluation of Eq. 2 for one word: s = sum_{i<m} (v[i] - vmin) B^i,
 // evaluated from the last digit down.
@@ -128,7 +114,7 @@ __global__ void __launch_bounds__(NT) poly_compress_block_scan(CompressArgs a) {
   const uint64_t P = s_prefix;
   for (uint32_t i = tid; i < nblk; i += NT) a.woff[b0 + i] = P + s_off[i];
   if (tile == sh.n_stiles - 1 && tid == 0) {
-    write_global_header(a.out, sh, P + total);
+    write_global_header_f(a.out, sh.width, sh.n, sh.block_len, sh.n_blocks, P + total);
     *a.compressed_bytes = 32 + 16 * sh.n_blocks + 8 * (P + total);
   }
 }

@@ -33,9 +33,6 @@ __host__ __device__ constexpr int t32min_u16(int K) {
        : 0;
 }
 
-#ifndef POLY_KW_FOLD
-#define POLY_KW_FOLD 0  // 1: the block minimum folded into the digit steps' addends (measured slower: cfg4 1390 -> 1326 GB/s)
-#endif
 
 template <int K>
 struct KCls {
@@ -173,26 +170,6 @@ __device__ __forceinline__ uint32_t unpack_group(const uint64_t* src, uint32_t g
       const uint64_t mid = lo2 + hi1;
       const uint64_t f = ((hi2 + (mid < lo2 ? 1ull : 0ull)) << 32) + (mid >> 32) + 1;
       uint32_t f0 = (uint32_t)f, f1 = (uint32_t)(f >> 32);
-#if POLY_KW_FOLD
-      // the minimum rides in the high word of each step's addend, so every
-      // digit comes out as its value (vmin + digit < 2^16: no carry out)
-      const uint64_t vm = (uint64_t)vmin << 32;
-#pragma unroll
-      for (int i = K - 1; i >= T; --i) {
-        const uint64_t t0 = (uint64_t)f0 * B;
-        const uint64_t t1 = (uint64_t)f1 * B + (vm | (uint32_t)(t0 >> 32));
-        d[i] = (uint32_t)(t1 >> 32);
-        f1 = (uint32_t)t1;
-        f0 = (uint32_t)t0;
-      }
-      uint32_t gg = f1 + 1;
-#pragma unroll
-      for (int i = T - 1; i >= 0; --i) {
-        const uint64_t p = (uint64_t)gg * B + vm;
-        d[i] = (uint32_t)(p >> 32);
-        gg = (uint32_t)p;
-      }
-#else
 #pragma unroll
       for (int i = K - 1; i >= T; --i) {
         const uint64_t t0 = (uint64_t)f0 * B;
@@ -208,7 +185,6 @@ __device__ __forceinline__ uint32_t unpack_group(const uint64_t* src, uint32_t g
         d[i] = (uint32_t)(p >> 32) + vmin;
         gg = (uint32_t)p;
       }
-#endif
     }
     if (j) {
 #pragma unroll

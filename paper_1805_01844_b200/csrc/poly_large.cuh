@@ -340,7 +340,9 @@ __device__ __forceinline__ uint32_t check_global_header_l(const LargeArgs& a, ui
   if (((h0.y >> 8) & 0xffu) != 0u || ((h0.y >> 16) & 0xffu) != sh.width || (h0.y >> 24) != 0u || n != sh.n ||
       h1.x != sh.block_len || h1.y != (uint32_t)sh.n_blocks)
     return POLY_ST_HEADER_MISMATCH;
-  if ((pb & 7) != 0 || a.in_bytes != 32 + 16 * sh.n_blocks + pb) return POLY_ST_LENGTH;
+  // overflow-safe: in_bytes must hold the headers before pb is compared with the rest
+  if ((pb & 7) != 0 || a.in_bytes < 32 + 16 * sh.n_blocks || pb != a.in_bytes - (32 + 16 * sh.n_blocks))
+    return POLY_ST_LENGTH;
   *pw = pb >> 3;
   return 0;
 }

@@ -56,6 +56,16 @@ __device__ __forceinline__ void trace_ev(uint32_t i, int e, uint64_t v = ~0ull) 
 #endif
 constexpr int NCW = POLY_NCW;      // consumer warps
 constexpr int PC = NCW * 32;       // consumer threads
+// Timing experiments (skip compute / the look-back / stores; the output is
+// then wrong) exist only in a separate variant library built with
+// -DPOLY_TIMING (profiles/); in the product library DBG(x) is the constant 0
+// and the experiment branches compile away.
+#ifdef POLY_TIMING
+#define DBG(a, bit) ((a).debug & (bit))
+#else
+#define DBG(a, bit) 0u
+#endif
+
 #ifndef POLY_NLB_MAX
 #define POLY_NLB_MAX 4
 #endif
@@ -109,7 +119,7 @@ struct PipeArgs {
   uint64_t* status;         // look-back words, one per tile
   uint32_t* ticket;
   uint32_t bulk;            // value array 16-byte aligned and tile_bytes % 16 == 0
-  uint32_t debug;           // timing experiments only (POLY_DEBUG): 1 skip compute, 2 skip look-back
+  uint32_t debug;           // POLY_TIMING builds only (read through DBG): 1 skip compute, 2 skip look-back, ...
   uint32_t nlb;             // look-back / writer warps in use
   uint32_t server;          // 1: the last CTA is the prefix server (see prefix_server)
   uint64_t t_begin, t_end;  // compress: the tiles of this launch (chunked host calls)
@@ -178,20 +188,8 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t tx) {
 #define POLY_SUSPEND_NS 0x989680u
 #endif
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity);
-#ifndef POLY_MAP0_JCAP
-#define POLY_MAP0_JCAP 0  // decompress map 0: full words per block decoded in-lane before the overflow round (0: all; 2 measured slower)
-#endif
-#ifndef POLY_MAP0_BULK_OUT
-#define POLY_MAP0_BULK_OUT 0  // decompress map 0: each group leaves staging by one TMA bulk store (measured slower than the copy)
-#endif
-#ifndef POLY_MAP1_CLAIM
-#define POLY_MAP1_CLAIM 0  // decompress map 1 with G = 1: blocks claimed from a counter (measured slower)
-#endif
 #ifndef POLY_CMP_WARP_RINGS
 #define POLY_CMP_WARP_RINGS 1  // compress map 0 (bpt = 1): per-warp word rings, no CTA scan
-#endif
-#ifndef POLY_MAP0_DYNAMIC
-#define POLY_MAP0_DYNAMIC 1  // decompress map 0: groups claimed from a counter (1) or by warp index (0)
 #endif
 #ifndef POLY_WAIT_MIN
 #define POLY_WAIT_MIN 32  // first sleep (ns) of a barrier poll
@@ -704,7 +702,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
         const uint32_t wex = warp_excl_scan(ww, &Wt);
         if (lane == 0) st_relaxed_u64(a.status + t, (t == 0 && !a.server ? FLAG_PRE : FLAG_AGG) | Wt);
         uint64_t P = 0;
-        if (t != 0 && !(a.debug & 2)) {
+        if (t != 0 && !DBG(a, 2)) {
           if (a.server) {
             P = wait_prefix(a.status, t);
           } else {
@@ -758,7 +756,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       }
       const uint64_t W = C.rec_W[r];
       uint64_t P = 0;
-      if (t != 0 && !(a.debug & 2)) {
+      if (t != 0 && !DBG(a, 2)) {
         if (a.server) {
           P = wait_prefix(a.status, t);
         } else {
@@ -834,7 +832,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       // concatenate the warp segments and publish the tile aggregate).
       const uint32_t b = ctid;
       uint32_t vmn = 0, bmm = 0, nwb = 0, kkb = 1;
-      if (b < nblk && !(a.debug & 1)) {
+      if (b < nblk && !DBG(a, 1)) {
         const uint32_t nb = min(L, nv - b * L);
         uint32_t mn, mx;
         block_minmax<V>(sv + (size_t)b * L, nb, mn, mx);
@@ -898,7 +896,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
     uint32_t vmin[BPT_MAX], bm1[BPT_MAX], nw[BPT_MAX], kk[BPT_MAX], off[BPT_MAX];
 
     // ---- a2, a3: block statistics, headers, in-tile word offsets
-    if (a.debug & 1) {
+    if (DBG(a, 1)) {
 #pragma unroll
       for (int q = 0; q < BPT_MAX; ++q) {
         vmin[q] = bm1[q] = nw[q] = off[q] = 0;
@@ -1068,7 +1066,9 @@ __device__ __forceinline__ uint32_t check_global_header_p(const PipeArgs& a, uin
   if (((h0.y >> 8) & 0xffu) != 0u || ((h0.y >> 16) & 0xffu) != sh.width || (h0.y >> 24) != 0u || n != sh.n ||
       h1.x != sh.block_len || h1.y != (uint32_t)sh.n_blocks)
     return POLY_ST_HEADER_MISMATCH;
-  if ((pb & 7) != 0 || a.in_bytes != 32 + 16 * sh.n_blocks + pb) return POLY_ST_LENGTH;
+  // overflow-safe: in_bytes must hold the headers before pb is compared with the rest
+  if ((pb & 7) != 0 || a.in_bytes < 32 + 16 * sh.n_blocks || pb != a.in_bytes - (32 + 16 * sh.n_blocks))
+    return POLY_ST_LENGTH;
   *pw = pb >> 3;
   return 0;
 }
@@ -1095,16 +1095,12 @@ __device__ __forceinline__ uint32_t fstep32v(uint32_t& g, uint32_t B, uint32_t v
   return d;
 }
 
-#ifndef POLY_DIGIT_UNROLL
-#define POLY_DIGIT_UNROLL 2  // digits per iteration of the step loops (2 or 4; 2 measured faster)
-#endif
 // The m top digits of a word (already premultiplied so they are its top
 // digits), written most significant first at o[0], o[-1], ...: n64 64-bit
 // steps, then n32 32-bit steps.
 template <typename V>
 __device__ __forceinline__ void digits_out(uint32_t f0, uint32_t f1, uint32_t add, uint32_t B, uint32_t vmin,
                                            int n64, int n32, V* o) {
-#if POLY_DIGIT_UNROLL == 2
 #pragma unroll 1
   for (; n64 >= 2; n64 -= 2, o -= 2) {
     const uint32_t d1 = fstep64v(f0, f1, B, vmin);
@@ -1125,73 +1121,6 @@ __device__ __forceinline__ void digits_out(uint32_t f0, uint32_t f1, uint32_t ad
     o[-1] = (V)d0;
   }
   if (n32) o[0] = (V)fstep32v(g, B, vmin);
-#else
-  // four digits per iteration (the step chains stay in registers), then singles
-#pragma unroll 1
-  for (; n64 >= 4; n64 -= 4, o -= 4) {
-    uint32_t d[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) d[u] = fstep64v(f0, f1, B, vmin);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) o[-u] = (V)d[u];
-  }
-#pragma unroll 1
-  for (; n64 > 0; --n64, --o) o[0] = (V)fstep64v(f0, f1, B, vmin);
-  uint32_t g = f1 + add;
-#pragma unroll 1
-  for (; n32 >= 4; n32 -= 4, o -= 4) {
-    uint32_t d[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) d[u] = fstep32v(g, B, vmin);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) o[-u] = (V)d[u];
-  }
-#pragma unroll 1
-  for (; n32 > 0; --n32, --o) o[0] = (V)fstep32v(g, B, vmin);
-#endif
-}
-
-#ifndef POLY_PAIR_DECODE
-#define POLY_PAIR_DECODE 0  // 1: decode a block's full words two at a time (measured slower)
-#endif
-// Two full words of one block at once (same B, k, t): the two digit chains
-// interleave, so a lane has two independent multiplies in flight.
-template <typename V>
-__device__ __forceinline__ void digits_out2(uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1, uint32_t add,
-                                            uint32_t B, uint32_t vmin, int n64, int n32, V* oa, V* ob) {
-#pragma unroll 1
-  for (; n64 >= 2; n64 -= 2, oa -= 2, ob -= 2) {
-    const uint32_t x1 = fstep64v(a0, a1, B, vmin);
-    const uint32_t y1 = fstep64v(b0, b1, B, vmin);
-    const uint32_t x0 = fstep64v(a0, a1, B, vmin);
-    const uint32_t y0 = fstep64v(b0, b1, B, vmin);
-    oa[0] = (V)x1;
-    ob[0] = (V)y1;
-    oa[-1] = (V)x0;
-    ob[-1] = (V)y0;
-  }
-  if (n64) {
-    oa[0] = (V)fstep64v(a0, a1, B, vmin);
-    ob[0] = (V)fstep64v(b0, b1, B, vmin);
-    --oa;
-    --ob;
-  }
-  uint32_t ga = a1 + add, gb = b1 + add;
-#pragma unroll 1
-  for (; n32 >= 2; n32 -= 2, oa -= 2, ob -= 2) {
-    const uint32_t x1 = fstep32v(ga, B, vmin);
-    const uint32_t y1 = fstep32v(gb, B, vmin);
-    const uint32_t x0 = fstep32v(ga, B, vmin);
-    const uint32_t y0 = fstep32v(gb, B, vmin);
-    oa[0] = (V)x1;
-    ob[0] = (V)y1;
-    oa[-1] = (V)x0;
-    ob[-1] = (V)y0;
-  }
-  if (n32) {
-    oa[0] = (V)fstep32v(ga, B, vmin);
-    ob[0] = (V)fstep32v(gb, B, vmin);
-  }
 }
 
 // One full-length block (nb = L, B <= CACHE_B, B < 2^32) from its cached
@@ -1213,19 +1142,6 @@ __device__ __forceinline__ uint32_t decode_block_ent(const uint64_t* src, uint32
   *extra = nfull - nin;
   V* o = dst + (k - 1);
   uint32_t j = 0;
-#if POLY_PAIR_DECODE
-#pragma unroll 1
-  for (; j + 2 <= nfull; j += 2, o += 2 * k) {  // full words in pairs
-    const uint64_t sa = src[j], sb = src[j + 1];
-    if (sa > Wmax || sb > Wmax) err = POLY_ST_RESIDUE;
-    const uint64_t ha1 = __umul64hi(sa, Rl), la2 = sa * Rh, ha2 = __umul64hi(sa, Rh), ma = la2 + ha1;
-    const uint64_t hb1 = __umul64hi(sb, Rl), lb2 = sb * Rh, hb2 = __umul64hi(sb, Rh), mb = lb2 + hb1;
-    const uint64_t fa = ((ha2 + (ma < la2 ? 1ull : 0ull)) << 32) + (ma >> 32) + add;
-    const uint64_t fb = ((hb2 + (mb < lb2 ? 1ull : 0ull)) << 32) + (mb >> 32) + add;
-    digits_out2<V>((uint32_t)fa, (uint32_t)(fa >> 32), (uint32_t)fb, (uint32_t)(fb >> 32), add, B, vmin,
-                   (int)(k - t), (int)t, o, o + k);
-  }
-#endif
 #pragma unroll 1
   for (; j < nin; ++j, o += k) {
     const uint64_t s = src[j];
@@ -1310,75 +1226,11 @@ __device__ __forceinline__ uint32_t decode_tail(const uint64_t* src, uint32_t j0
   return err;
 }
 
-#ifndef POLY_BIN_STAGING
-#define POLY_BIN_STAGING 4  // map 2: decoded tiles staged for their bulk stores (<= 4)
-#endif
-// Binned map 0 (MAP 2): a counting sort of a tile's blocks by k, so that the
-// 32 lanes of a consumer warp decode blocks with the same word count and digit
-// loops (the order within a bucket is free: a block's output position is its
-// own).  OFF[i] = (in-tile word offset << 12) | block of slot i; bins = 128
-// words of the stage after OFF (plan_pipe_n).  Shared-memory atomics rank
-// the blocks; run by the tile's look-back warp while its payload lands.
-template <int QN>
-__device__ __forceinline__ void bin_sort(const uint4* H, uint32_t* OFF, uint32_t* bins, uint32_t nblk, uint32_t L,
-                                         uint32_t nv, const BaseCache& bc, uint32_t lane) {
-  uint32_t off[QN], kp[(QN + 3) / 4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) bins[32 * j + lane] = 0;
-  __syncwarp();
-  uint32_t Wt = 0;
-#pragma unroll
-  for (int q = 0; q < QN; ++q) {
-    const uint32_t b = 32 * q + lane;
-    uint32_t x = 0, key = 127u;  // 127: no block
-    if (b < nblk) {
-      const uint4 h = H[b];
-      x = min(h.w, 0xfffffu);
-      key = 0u;  // general path
-      if (h.x == CODEC_BASIC && h.z != 0 && h.z < CACHE_B && (b + 1) * L <= nv)
-        key = bc.E[h.z + 1].meta & 0xffu;  // k of a full-length cached base
-      atomicAdd(&bins[key], 1u);
-    }
-    uint32_t v = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
-      if (lane >= o) v += y;
-    }
-    off[q] = Wt + v - x;
-    Wt += __shfl_sync(0xffffffffu, v, 31);
-    if (q % 4 == 0) kp[q / 4] = 0;
-    kp[q / 4] |= key << (8 * (q % 4));
-  }
-  __syncwarp();
-  // exclusive scan of bins 0..63 (k <= 64: bin 64 only for B = 2, L >= 64... kept in range below)
-  uint32_t carry = 0;
-#pragma unroll
-  for (int j = 0; j < 3; ++j) {
-    const uint32_t c = bins[32 * j + lane];
-    uint32_t v = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
-      if (lane >= o) v += y;
-    }
-    __syncwarp();
-    bins[32 * j + lane] = carry + v - c;
-    carry += __shfl_sync(0xffffffffu, v, 31);
-  }
-  __syncwarp();
-#pragma unroll
-  for (int q = 0; q < QN; ++q) {
-    const uint32_t key = (kp[q / 4] >> (8 * (q % 4))) & 0xffu;
-    if (key != 127u) OFF[atomicAdd(&bins[key], 1u)] = (off[q] << 12) | (32u * q + lane);
-  }
-}
-
 template <typename V, int MAP, int NW>
 __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_decompress_pipe(PipeArgs a) {
   constexpr int NCW = NW, PC = NW * 32, PT = PC + 32 * (2 + NLB_MAX);
   constexpr int W_PROD = NCW, W_WRIT = NCW + 1, W_HSUM = NCW + 2, W_LBX = NCW + 3;
-  constexpr uint32_t NTS = MAP == 2 ? POLY_BIN_STAGING : 2;  // staging tiles (maps 1, 2)
+  constexpr uint32_t NTS = 2;  // staging tiles (map 1)
   (void)W_HSUM;
   (void)W_LBX;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -1396,7 +1248,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
     for (uint32_t s = 0; s < S; ++s) {
       mbar_init(&C.hbar[s], 1);
       mbar_init(&C.aggr[s], 1);
-      mbar_init(&C.full_in[s], MAP == 2 ? 2 : 1);  // map 2: + the look-back warp's sort
+      mbar_init(&C.full_in[s], 1);
       mbar_init(&C.empty_in[s], NCW);
       C.done_cnt[s] = 0;
       C.gnext[s] = 0;
@@ -1484,7 +1336,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       // consumers reject such a block and the look-back warp such a tile.
       const uint32_t* Hw = reinterpret_cast<const uint32_t*>(H) + 3;
       uint32_t Wt = 0;
-      if (MAP == 0 || MAP == 2) {
+      if (MAP == 0) {
         // map 0: only each 32-block group's offset (OFF[g]); a consumer warp
         // scans within its group.  One warp reduction per group.  (Map 2: the
         // tile's sum only; its look-back warp rewrites OFF with sorted slots.)
@@ -1555,13 +1407,12 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       const uint64_t t = C.tkt[s];
       if (t == TILE_NONE) {
         if (lane == 0) mbar_arrive(&C.full_in[s]);
-        if (MAP == 2 && lane == 0) mbar_arrive(&C.full_in[s]);
         break;
       }
       if (lane == 0) TRACE(i, 3);
       const uint64_t W = C.W[s];
       uint64_t P = 0;
-      if (a.debug & 2) {
+      if (DBG(a, 2)) {
         P = min(t * (pw / sh.n_tiles), pw - min(pw, W));
       } else if (t != 0) {
         if (a.server) {
@@ -1573,13 +1424,13 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       }
       if (lane == 0) TRACE(i, 4);
       uint32_t e = 0;
-      uint64_t wl = (a.debug & 16) ? 0 : W;
+      uint64_t wl = DBG(a, 16) ? 0 : W;
       if (W > sh.words_cap || P + W > pw) {
         e = POLY_ST_LENGTH;
         wl = 0;
       }
       if (t == sh.n_tiles - 1 && P + W != pw) e |= POLY_ST_LENGTH;
-      if (a.debug & 2) e = 0;
+      if (DBG(a, 2)) e = 0;
       if (lane == 0) {
         C.P[s] = P;
         C.err[s] = e;
@@ -1624,32 +1475,6 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
         }
       }
       __syncwarp();
-      if (MAP == 2) {  // the tile's sorted slots, while its payload lands
-        const uint8_t* st = smem + sh.o_in + (size_t)s * sh.in_stride;
-        const uint64_t b0 = t * sh.TB;
-        const uint32_t nblk = (uint32_t)min((uint64_t)sh.TB, sh.n_blocks - b0);
-        const uint32_t nv = (uint32_t)(min(sh.n, b0 * sh.Le + (uint64_t)sh.TB * sh.Le) - b0 * sh.Le);
-        uint32_t* OFFw = reinterpret_cast<uint32_t*>(smem + sh.o_in + (size_t)s * sh.in_stride + sh.o_off);
-        if (a.debug & 32) {  // timing experiment: identity order (valid, unsorted)
-          uint32_t Wt = 0;
-          for (uint32_t r0 = 0; r0 < nblk; r0 += 32) {
-            const uint32_t b = r0 + lane;
-            const uint32_t x = b < nblk ? min(reinterpret_cast<const uint4*>(st)[b].w, 0xfffffu) : 0u;
-            uint32_t v = x;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
-              if (lane >= o) v += y;
-            }
-            if (b < nblk) OFFw[b] = ((Wt + v - x) << 12) | b;
-            Wt += __shfl_sync(0xffffffffu, v, 31);
-          }
-        } else {
-          bin_sort<(NW + 1) / 2>(reinterpret_cast<const uint4*>(st), OFFw, OFFw + sh.TB, nblk, (uint32_t)sh.Le, nv, bc, lane);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&C.full_in[s]);
-      }
     }
     return;
   }
@@ -1664,7 +1489,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       if (bytes == ~0u) break;
       uint8_t* og = C.t_og[q];
       const uint8_t* src = smem + sh.o_out + (size_t)q * sh.out_stride;
-      if (bytes && !(a.debug & 8)) {
+      if (bytes && !DBG(a, 8)) {
         if (a.bulk) {
           const uint32_t b16 = bytes & ~15u;  // the tile starts 16-byte aligned
           if (lane == 0 && b16) bulk_s2g(og, src, b16);
@@ -1692,7 +1517,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
   // all NCW warps have arrived.
   const uint32_t L = (uint32_t)sh.Le;
   uint32_t err = 0;
-  const bool bst = a.bulk && !(a.debug & 4);
+  const bool bst = a.bulk && !DBG(a, 4);
   for (uint32_t s = 0, ph = 0, s2 = 0, it = 0;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0), s2 = (s2 + 1 == NTS) ? 0 : s2 + 1, ++it) {
     mbar_wait_dec(&C.full_in[s], ph);
     if (lane == 0 && warp == 0) TRACE(it, 6);
@@ -1730,79 +1555,19 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
 #pragma unroll 1
       for (uint32_t gi = 0;; ++gi) {
         uint32_t g = 0;
-#if POLY_MAP0_DYNAMIC
         if (lane == 0) g = atomicAdd(&C.gnext[s], 1u);
         g = __shfl_sync(0xffffffffu, g, 0);
-#else
-        g = warp + gi * NCW;  // static: group = warp (TB = 32 NCW: one group per warp and tile)
-#endif
         if (g >= ngrp) break;
         const uint32_t g0 = g * 32, b = g0 + lane;
         const uint4 h = b < nblk ? H[b] : make_uint4(0, 0, 0, 0);
         uint32_t tot;
         const uint32_t ex = warp_excl_scan(min(h.w, 0xfffffu), &tot);
-#if POLY_MAP0_BULK_OUT
-        if (bst) {  // the staging buffer's previous bulk store has read it
-          if (lane == 0) bulk_wait_read<0>();
-          __syncwarp();
-        }
-#endif
-#if POLY_MAP0_JCAP
-        // the first JCAP full words of every block per lane; the rest (blocks
-        // of small k: more words) spread over the warp's lanes afterwards, so
-        // one such block no longer holds the whole warp for extra rounds
-        uint32_t xw = 0;
-        if (b < nblk && !terr && !(a.debug & 1))
-          err |= decode_block0<V>(h, PAY + OFF[g] + ex, min(L, nv - b * L), L, sh.width, bc,
-                                  ob + (size_t)lane * L, POLY_MAP0_JCAP, &xw);
-        uint32_t totx;
-        const uint32_t exx = warp_excl_scan(xw, &totx);
-#pragma unroll 1
-        for (uint32_t r0 = 0; r0 < totx; r0 += 32) {
-          const uint32_t q = r0 + lane;
-          int o = 0;  // the last lane whose first overflow word is <= q
-#pragma unroll
-          for (int st = 16; st >= 1; st >>= 1) {
-            const uint32_t v = __shfl_sync(0xffffffffu, exx, o + st);
-            if (v <= q) o += st;
-          }
-          const uint32_t jx = POLY_MAP0_JCAP + q - __shfl_sync(0xffffffffu, exx, o);
-          const uint32_t exo = __shfl_sync(0xffffffffu, ex, o);
-          if (q < totx) {
-            const uint4 ho = H[g0 + o];
-            const uint32_t Bo = ho.z + 1;
-            const DecEnt& eo = bc.E[Bo];
-            const uint32_t meta = eo.meta, k = meta & 0xffu, t = (meta >> 16) & 0xffu;
-            const uint32_t add = ((meta >> 8) & 0xffu) ? 0u : 1u;
-            const uint64_t sw = PAY[OFF[g] + exo + jx];
-            if (sw > eo.Wmax) err |= POLY_ST_RESIDUE;
-            const uint64_t Rl = eo.Rl, Rh = eo.Rh;
-            const uint64_t hi1 = __umul64hi(sw, Rl), lo2 = sw * Rh, hi2 = __umul64hi(sw, Rh), mid = lo2 + hi1;
-            const uint64_t f = ((hi2 + (mid < lo2 ? 1ull : 0ull)) << 32) + (mid >> 32) + add;
-            digits_out<V>((uint32_t)f, (uint32_t)(f >> 32), add, Bo, ho.y, (int)(k - t), (int)t,
-                          ob + (size_t)o * L + jx * k + (k - 1));
-          }
-        }
-#else
-        if (b < nblk && !terr && !(a.debug & 1))
+        if (b < nblk && !terr && !DBG(a, 1))
           err |= decode_block0<V>(h, PAY + OFF[g] + ex, min(L, nv - b * L), L, sh.width, bc, ob + (size_t)lane * L);
-#endif
         __syncwarp();
         const uint32_t bytes = min(nv * sh.vb - g0 * L * sh.vb, gb);
         uint8_t* dst = og + (size_t)g0 * L * sh.vb;
-        if (!(a.debug & 8)) {
-#if POLY_MAP0_BULK_OUT
-          if (bst) {  // one bulk store (TMA) of the group; waited for before the buffer is rewritten
-            fence_proxy_async_smem();
-            __syncwarp();
-            const uint32_t b16 = bytes & ~15u;
-            if (lane == 0 && b16) {
-              bulk_s2g(dst, ob8, b16);
-              bulk_commit();
-            }
-            for (uint32_t i = b16 + lane; i < bytes; i += 32) dst[i] = ob8[i];
-          } else
-#endif
+        if (!DBG(a, 8)) {
           if (a.bulk) {
             // 16-byte copies, lane-strided (a group is at most 4 KiB: <= 8 per lane)
             const uint32_t n16 = bytes >> 4;
@@ -1818,48 +1583,16 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
         }
         __syncwarp();
       }
-    } else if (MAP == 2) {
-      // binned map 0: groups of 32 sorted slots (blocks of equal k) claimed
-      // dynamically; each lane decodes its block into the tile's staging
-      // buffer at the block's own position; the tile store warp bulk-stores
-      // the tile once every warp is done with it (as map 1).
-      mbar_wait_dec(&C.tfree[s2], ((it / NTS) & 1u) ^ 1u);
-      const uint32_t ngrp = (nblk + 31) / 32;
-#pragma unroll 1
-      for (;;) {
-        uint32_t g = 0;
-        if (lane == 0) g = atomicAdd(&C.gnext[s], 1u);
-        g = __shfl_sync(0xffffffffu, g, 0);
-        if (g >= ngrp) break;
-        const uint32_t i = g * 32 + lane;
-        if (i < nblk && !terr && !(a.debug & 1)) {
-          const uint32_t e = OFF[i];
-          const uint32_t b = e & 0xfffu;
-          err |= decode_block0<V>(H[b], PAY + (e >> 12), min(L, nv - b * L), L, sh.width, bc, ob + (size_t)b * L);
-        }
-      }
-      if (bst) fence_proxy_async_smem();
-      if (warp == 0 && lane == 0) {
-        C.t_og[s2] = og;
-        C.t_bytes[s2] = nv * sh.vb;
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&C.tfull[s2]);
     } else {
       // map 1: part p of a block (G parts) decodes one contiguous range of the
       // block's values into the tile's staging buffer; the tile store warp
       // bulk-stores the whole tile once every warp is done, so no warp waits
       // for another (the buffer was freed by the store of two tiles ago).
       mbar_wait_dec(&C.tfree[s2], ((it / NTS) & 1u) ^ 1u);
-      const bool claim = sh.G == 1 && POLY_MAP1_CLAIM;
       const uint32_t G = sh.G;
 #pragma unroll 1
       for (uint32_t gi = 0;; ++gi) {
-        uint32_t seg = warp + gi * NCW;
-        if (claim) {
-          if (lane == 0) seg = atomicAdd(&C.gnext[s], 1u);
-          seg = __shfl_sync(0xffffffffu, seg, 0);
-        }
+        const uint32_t seg = warp + gi * NCW;
         if (seg >= sh.TB * G) break;
         const uint32_t b = seg / G, part = seg % G;
         if (b >= nblk) break;
@@ -1868,7 +1601,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
         V* dst = ob + (size_t)b * L;
         uint32_t vlo = (uint32_t)(((uint64_t)nb * part / G) & ~7ull), vhi = part + 1 == G ? nb
                                                                          : (uint32_t)(((uint64_t)nb * (part + 1) / G) & ~7ull);
-        if (!terr && !(a.debug & 1)) {
+        if (!terr && !DBG(a, 1)) {
           const uint32_t k = (h.x == CODEC_BASIC && h.z != 0) ? dk_of(bc, (uint64_t)h.z + 1) : 1u;
           const uint32_t e = check_block_hdr(h, nb, sh.width, k);
           err |= e;
@@ -1933,9 +1666,6 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       mbar_arrive(&C.empty_in[s]);
     }
   }
-#if POLY_MAP0_BULK_OUT
-  if (MAP == 0 && bst && lane == 0) bulk_wait_all<0>();  // staging stays valid until the stores read it
-#endif
   err = __reduce_or_sync(0xffffffffu, err);
   if (lane == 0 && err) atomicOr(a.status_out, err);
 }

@@ -34,7 +34,7 @@ POLY_ST_LENGTH = 128
 
 EXPORTS = ["poly_version", "poly_status_string", "poly_init", "poly_max_compressed_bytes",
            "poly_workspace_bytes", "poly_compress", "poly_read_header", "poly_decompress",
-           "poly_compress_host", "poly_decompress_host", "poly_launches_per_call"]
+           "poly_compress_host", "poly_decompress_host", "poly_launches_per_call", "poly_tables_ok"]
 
 
 class PolyError(RuntimeError):
@@ -66,6 +66,8 @@ def load_library(path: str = LIB_PATH):
     L.poly_max_compressed_bytes.argtypes = [u64, i32, u64]
     L.poly_workspace_bytes.restype = u64
     L.poly_workspace_bytes.argtypes = [u64, i32, u64]
+    L.poly_tables_ok.restype = i32
+    L.poly_tables_ok.argtypes = []
     L.poly_launches_per_call.restype = i32
     L.poly_launches_per_call.argtypes = [u64, i32, u64, i32]
     L.poly_compress.restype = i32
@@ -110,6 +112,11 @@ def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
 def _check(rc: int, what: str):
     if rc != POLY_OK:
         raise PolyError(rc, what)
+
+
+def poly_tables_ok() -> bool:
+    """Host-only self-check of the decoder tables (include/poly.h)."""
+    return bool(load_library().poly_tables_ok())
 
 
 def poly_version() -> int:

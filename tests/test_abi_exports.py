@@ -98,3 +98,43 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", src).replace("oracle/", ""), f
+
+
+def test_decoder_tables_selfcheck(lib):
+    """The host builds the per-base decoder constants with exact integers and
+    checks the preconditions of DESIGN.md Sec. 5.3, including the compile-time
+    T32MIN[K] switch points of the k-specialised decoders (poly_kword.cuh)."""
+    assert polycomp.poly_tables_ok()
+
+
+def test_t32min_table_matches_exact_integers():
+    """Independent of the library: T32MIN[K] = min over non-power-of-two
+    B <= 65536 with capacity K of t32(B) = max{t <= min(k, h) :
+    2^32 B^k + B^k + 2^64 B^t <= 2^96}, recomputed with Python integers and
+    compared with the constants compiled into poly_kword.cuh."""
+    src = open(os.path.join(ROOT, "paper_1805_01844_b200", "csrc", "poly_kword.cuh")).read()
+    body = src[src.index("constexpr int t32min_u16(int K)"):]
+    body = body[:body.index(";")]
+    table = {int(k): int(v) for k, v in re.findall(r"K == (\d+) \? (\d+)", body)}
+    lo = {}
+    for B in range(3, 65537):
+        if B & (B - 1) == 0:
+            continue
+        k, p = 0, 1
+        while p * B <= 1 << 64:
+            p *= B
+            k += 1
+        h, q = 0, 1
+        while q * B <= 1 << 32:
+            q *= B
+            h += 1
+        t, bt = 0, 1
+        for tt in range(1, min(k, h) + 1):
+            bt *= B
+            if (p << 32) + p + (bt << 64) <= 1 << 96:
+                t = tt
+            else:
+                break
+        lo[k] = min(lo.get(k, 99), t)
+    for K, v in table.items():
+        assert lo[K] == v, (K, lo[K], v)

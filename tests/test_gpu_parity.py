@@ -99,18 +99,60 @@ def test_random_small_shapes(oracle_lib):
         check_case(oracle_lib, x.astype(np.uint16 if w == 16 else np.uint32), L)
 
 
-def test_every_u16_base_decodes(oracle_lib):
-    """Each block of 64 values spans exactly base B (0 and B-1 present), for
-    every B in 2..65536 in turn: exercises every table entry of both sides."""
+def worst_case_blocks(Bs, L, rng):
+    """One block of L values per base B (u16), each holding the words that
+    stress the decoder: 0 and B-1 (so the block's base is
+    exactly B), a whole word of digits B-1 (the largest full word B^k - 1), and
+    a top word of digits B-1 (B^m - 1, the largest partial word); the rest is
+    uniform.  Returns the u16 array."""
+    Bs = np.asarray(Bs, dtype=np.int64)
+    d = rng.integers(0, 1 << 62, size=(Bs.size, L), dtype=np.int64) % Bs[:, None]
+    for r, B in enumerate(Bs.tolist()):
+        k = capacity_u64(B)
+        m = L % k or k
+        d[r, L - m:] = B - 1                # top word: every digit B - 1
+        if L >= 2 * k:
+            d[r, k:2 * k] = B - 1           # word 1: every digit B - 1
+        d[r, 0] = 0
+        d[r, 1] = B - 1
+    off = rng.integers(0, 1 << 16, size=Bs.size) % (65537 - Bs)
+    return (d + off[:, None]).astype(np.uint16).reshape(-1)
+
+
+def capacity_u64(B: int) -> int:
+    k, p = 0, 1
+    while p * B <= 1 << 64:
+        p *= B
+        k += 1
+    return k
+
+
+def test_every_u16_base_worst_words_map0(oracle_lib):
+    """Every B in 2..65536, one 64-value block each (map 0: one lane per
+    block), with the worst-case words of every base."""
     rng = np.random.default_rng(5)
-    B = np.arange(2, 65537, dtype=np.int64)
-    L = 64
-    d = rng.integers(0, 1 << 62, size=(B.size, L), dtype=np.int64) % B[:, None]
-    d[:, 0] = 0
-    d[:, 1] = B - 1
-    off = rng.integers(0, 65536, size=B.size) % (65537 - B)
-    x = (d + off[:, None]).astype(np.uint16).reshape(-1)
-    check_case(oracle_lib, x, L)
+    x = worst_case_blocks(np.arange(2, 65537), 64, rng)
+    check_case(oracle_lib, x, 64)
+
+
+def test_every_u16_base_worst_words_map1(oracle_lib):
+    """Every B in 2..65536, one 1024-value block each: the map-1 decoders
+    (k-specialised unrolled group codecs for the u16 capacities, with their
+    compile-time T32MIN switch points) see every base with its worst words."""
+    rng = np.random.default_rng(6)
+    x = worst_case_blocks(np.arange(2, 65537), 1024, rng)
+    check_case(oracle_lib, x, 1024)
+
+
+def test_u16_bases_worst_words_large_blocks(oracle_lib):
+    """The large-block pipeline (blocks > 32 KiB, >= 256 blocks): every k
+    threshold base and its neighbours, powers of two and a spread of others."""
+    rng = np.random.default_rng(7)
+    th = [2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 16, 17, 19, 20, 23, 24, 30, 31, 40, 41, 56, 57, 84, 85,
+          138, 139, 256, 257, 565, 566, 1625, 1626, 7131, 7132, 65535, 65536]
+    Bs = sorted(set(th + [int(b) for b in np.unique(np.geomspace(2, 65536, 260).astype(np.int64))]))
+    x = worst_case_blocks(Bs, 17000, rng)
+    check_case(oracle_lib, x, 17000)
 
 
 def test_large_bases_u32(oracle_lib):
@@ -120,7 +162,10 @@ def test_large_bases_u32(oracle_lib):
     blocks = []
     for B in Bs:
         blk = rng.integers(0, B, size=77, dtype=np.uint64)
+        k = capacity_u64(B)
         blk[0], blk[1] = 0, B - 1
+        blk[k:2 * k] = B - 1                # a full word of digits B - 1
+        blk[77 - (77 % k or k):] = B - 1    # the top word: digits B - 1
         blocks.append(blk)
     x = np.concatenate(blocks).astype(np.uint32)
     check_case(oracle_lib, x, 77)
@@ -248,16 +293,9 @@ def _pipe_cases():
     ]
 
 
-@pytest.mark.parametrize("env", [{}, {"POLY_SERVER": "0"}, {"POLY_LB": "1"}, {"POLY_LB": "4"},
-                                 {"POLY_SERVER": "0", "POLY_LB": "3"}, {"POLY_BIN": "1"},
-                                 {"POLY_BIN": "1", "POLY_DEBUG": "32"}])
-def test_prefix_and_warp_variants(oracle_lib, env, monkeypatch):
-    """The tile-prefix variants (prefix-server CTA or in-worker look-back),
-    the look-back / writer warp counts and the binned map-0 decoder (blocks
-    sorted by k; POLY_DEBUG=32: its identity order), read at each launch, give
-    the same bytes."""
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
+def test_pipeline_shapes(oracle_lib):
+    """The pipeline cases of both maps, u16 and u32, ragged tails, the shared
+    compress word ring and the large-block pipeline, each against the oracle."""
     for x, L in _pipe_cases():
         check_case(oracle_lib, x, L)
 
@@ -276,30 +314,31 @@ def test_repeat_determinism(oracle_lib):
                                   .numpy().view(x.dtype), x)
 
 
-@pytest.mark.parametrize("serial", [False, True])
-def test_host_calls(oracle_lib, serial, monkeypatch):
+def test_host_calls(oracle_lib):
     """poly_compress_host / poly_decompress_host (pinned host buffers): the
-    chunked, copy-overlapped compress path and the serial one give the oracle's
-    bytes, and the round trip returns the values."""
-    if serial:
-        monkeypatch.setenv("POLY_HOST_SERIAL", "1")
+    chunked, copy-overlapped compress path (>= 16 tiles) and the serial one
+    (few tiles, u32, large blocks) give the oracle's bytes, and the round trip
+    returns the values."""
     rng = np.random.default_rng(99)
     for x, L in [(rng.integers(240, 275, 30 * 30000).astype(np.uint16), 30),
-                 (rng.integers(1900, 2100, 1024 * 700 + 5).astype(np.uint16), 1024)]:
-        dt = 16
+                 (rng.integers(1900, 2100, 1024 * 700 + 5).astype(np.uint16), 1024),
+                 (rng.integers(240, 275, 30 * 300).astype(np.uint16), 30),
+                 (rng.integers(0, 70000, 40000 * 300 + 3).astype(np.uint32), 40000)]:
+        dt = 16 if x.dtype == np.uint16 else 32
         n = x.size
-        h_in = torch.from_numpy(x.view(np.int16).copy()).view(torch.uint16).pin_memory()
+        h_in = torch.from_numpy(x.view(np.int16 if dt == 16 else np.int32).copy()).view(
+            torch.uint16 if dt == 16 else torch.uint32).pin_memory()
         cap = pc.poly_max_compressed_bytes(n, dt, L)
-        d_in = torch.empty(max(cap, 2 * n), dtype=torch.uint8, device="cuda")
-        d_out = torch.empty(max(cap, 2 * n), dtype=torch.uint8, device="cuda")
+        d_in = torch.empty(max(cap, n * dt // 8), dtype=torch.uint8, device="cuda")
+        d_out = torch.empty(max(cap, n * dt // 8), dtype=torch.uint8, device="cuda")
         ws = pc.alloc_workspace(n, dt, L, d_in.device)
         h_stream = torch.empty(cap, dtype=torch.uint8).pin_memory()
         nb = pc.poly_compress_host(h_in, L, d_in, d_out, ws, h_stream)
         assert h_stream[:nb].numpy().tobytes() == oracle_lib.compress(x, L)
-        h_out = torch.empty(n, dtype=torch.uint16).pin_memory()
+        h_out = torch.empty(n, dtype=torch.uint16 if dt == 16 else torch.uint32).pin_memory()
         st = pc.poly_decompress_host(h_stream, nb, dt, n, L, d_in, d_out, ws, h_out)
         assert st == 0
-        assert np.array_equal(h_out.view(torch.int16).numpy().view(np.uint16), x)
+        assert np.array_equal(h_out.view(torch.int16 if dt == 16 else torch.int32).numpy().view(x.dtype), x)
 
 
 @pytest.mark.parametrize("cfg", [1, 2])
