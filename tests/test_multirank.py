@@ -29,7 +29,7 @@ def _worker(rank, world, port, q):
     import torch.distributed as dist
 
     class A:  # the subset of bench arguments the reference arm reads
-        gpus, steps, warmup, config, cpu_seconds = world, 1, 1, 2, 0.05
+        gpus, steps, warmup, config, ref_seconds, scale = world, 1, 1, 2, 1.0, 0.001
 
     r, w, _ = bench.dist_init(A)
     out = {"rank": r, "world": w, "backend": dist.get_backend()}
