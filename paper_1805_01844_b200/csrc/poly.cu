@@ -182,6 +182,10 @@ poly_status_t ensure_init(int dev) {
   set_smem_attr(poly_compress_pack<uint16_t>, large_smem_pack<uint16_t>());
   set_smem_attr(poly_compress_pack<uint32_t>, large_smem_pack<uint32_t>());
   set_smem_attr(poly_decompress_unpack<uint16_t>, large_smem_unpack<uint16_t>());
+  set_smem_attr(poly_decompress_large1<uint16_t>, large_smem_unpack<uint16_t>());
+  set_smem_attr(poly_decompress_large1<uint32_t>, large_smem_unpack<uint32_t>());
+  set_smem_attr(poly_compress_large1<uint16_t>, large_smem_pack<uint16_t>());
+  set_smem_attr(poly_compress_large1<uint32_t>, large_smem_pack<uint32_t>());
   set_smem_attr(poly_decompress_unpack<uint32_t>, large_smem_unpack<uint32_t>());
   if (e == cudaSuccess) e = cudaGetLastError();
   if (cur != dev) cudaSetDevice(cur);
@@ -380,13 +384,23 @@ WsLayout ws_layout(const Shape& sh, Regime rg) {
   if (rg == PIPE || rg == LARGE2) {
     L.total = 64 + 8 * sh.n_chunks;
   } else {
+    // bmin / bmax: per-block running min / max (three-kernel path) or per-chunk
+    // partials (single-launch path, poly_compress_large1)
+    const uint64_t nmm = std::max(sh.n_blocks, sh.n_chunks);
     L.bmin_off = (64 + 8 * sh.n_stiles + 15) / 16 * 16;
-    L.bmax_off = (L.bmin_off + 4 * sh.n_blocks + 15) / 16 * 16;
-    L.woff_off = (L.bmax_off + 4 * sh.n_blocks + 15) / 16 * 16;
+    L.bmax_off = (L.bmin_off + 4 * nmm + 15) / 16 * 16;
+    L.woff_off = (L.bmax_off + 4 * nmm + 15) / 16 * 16;
     L.total = L.woff_off + 8 * sh.n_blocks;
   }
   return L;
 }
+
+// The LARGE regime in one launch per call (poly_compress_large1 /
+// poly_decompress_large1): a few blocks and chunks (cfg1: one 2 MiB block).
+bool large1_compress(const Shape& sh) {
+  return sh.n_blocks <= LARGE1C_MAX_BLOCKS && sh.n_chunks <= LARGE1C_MAX_CHUNKS;
+}
+bool large1_decompress(const Shape& sh) { return sh.n_blocks <= LARGE1_MAX_BLOCKS; }
 
 int current_device() {
   int d = 0;
@@ -607,7 +621,8 @@ int poly_launches_per_call(uint64_t n, poly_dtype_t dt, uint64_t block_size, int
   Regime rg;
   if (!plan(n, (uint32_t)dt, block_size, sh, rg)) return 0;
   if (rg == PIPE || rg == LARGE2) return 1;
-  return decompress ? 2 : 3;
+  if (decompress) return large1_decompress(sh) ? 1 : 2;
+  return large1_compress(sh) ? 1 : 3;
 }
 
 poly_status_t poly_compress(const void* d_in, uint64_t n, poly_dtype_t dt, uint64_t block_size,
@@ -663,6 +678,14 @@ poly_status_t poly_compress(const void* d_in, uint64_t n, poly_dtype_t dt, uint6
     a.bmax = reinterpret_cast<uint32_t*>(ws + W.bmax_off);
     a.woff = reinterpret_cast<uint64_t*>(ws + W.woff_off);
     cudaMemsetAsync(ws, 0, W.bmin_off, s);
+    if (large1_compress(sh)) {  // one cooperative launch (grid barrier inside)
+      auto k = dt == POLY_U16 ? poly_compress_large1<uint16_t> : poly_compress_large1<uint32_t>;
+      const uint32_t smem = dt == POLY_U16 ? large_smem_pack<uint16_t>() : large_smem_pack<uint32_t>();
+      const int grid = pipe_grid(k, smem, sh.n_chunks, dev, NT);
+      launch_k(k, grid, NT, smem, s, true, a);
+      if (cudaGetLastError() != cudaSuccess) return POLY_ERR_CUDA;
+      return POLY_OK;
+    }
     cudaMemsetAsync(a.bmin, 0xff, 4 * sh.n_blocks, s);
     cudaMemsetAsync(a.bmax, 0, 4 * sh.n_blocks, s);
     const int gr = grid_for(sh.n_chunks, dev);
@@ -751,8 +774,16 @@ poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_
     launch_decompress_pipe(sh, dt, a.in, compressed_bytes, d_out, d_status, ws, W, 0, ~0ull, s, dev);
   } else {
     a.woff = reinterpret_cast<uint64_t*>(ws + W.woff_off);
-    cudaMemsetAsync(ws, 0, W.bmin_off, s);
     const int gr = grid_for(sh.n_chunks, dev);
+    if (large1_decompress(sh)) {  // one launch: every CTA scans the few headers itself
+      if (dt == POLY_U16)
+        poly_decompress_large1<uint16_t><<<gr, NT, large_smem_unpack<uint16_t>(), s>>>(a);
+      else
+        poly_decompress_large1<uint32_t><<<gr, NT, large_smem_unpack<uint32_t>(), s>>>(a);
+      if (cudaGetLastError() != cudaSuccess) return POLY_ERR_CUDA;
+      return POLY_OK;
+    }
+    cudaMemsetAsync(ws, 0, W.bmin_off, s);
     poly_decompress_block_scan<<<(unsigned)sh.n_stiles, NT, 0, s>>>(a);
     if (dt == POLY_U16)
       poly_decompress_unpack<uint16_t><<<gr, NT, large_smem_unpack<uint16_t>(), s>>>(a);

@@ -182,4 +182,94 @@ __global__ void __launch_bounds__(NT) poly_decompress_unpack(DecompressArgs a) {
   if (tid == 0 && s_err) atomicOr(a.status_out, s_err);
 }
 
+// ------------------------------------------------------------ single launch
+// A few huge blocks in ONE launch (cfg1: one block of the whole array): every
+// CTA validates the headers and scans the blocks' n_words into its own
+// shared-memory offsets (n_blocks <= LARGE1_MAX_BLOCKS), then decodes its
+// chunks as poly_decompress_unpack does -- no offset kernel, no workspace.
+constexpr uint32_t LARGE1_MAX_BLOCKS = 256;
+constexpr uint32_t LARGE1_MAX_CHUNKS = 2048;
+
+template <typename V>
+__global__ void __launch_bounds__(NT) poly_decompress_large1(DecompressArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  V* s_out = reinterpret_cast<V*>(smem);
+  uint64_t* s_words = reinterpret_cast<uint64_t*>(smem + 16 * ((CH_VALUES + 64) * sizeof(V) / 16 + 1));
+  __shared__ uint64_t s_nw[LARGE1_MAX_BLOCKS], s_off[LARGE1_MAX_BLOCKS], s_warp[NWARP];
+  __shared__ DecConst s_c;
+  __shared__ uint32_t s_err, s_bad;
+  __shared__ uint64_t s_pw;
+  const Shape& sh = a.sh;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    uint64_t pw = 0;
+    s_bad = check_global_header(a, &pw);
+    s_pw = pw;
+    s_err = 0;
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (blockIdx.x == 0 && tid == 0) atomicOr(a.status_out, s_bad);
+    return;
+  }
+  const uint64_t payload_words = s_pw;
+  const uint4* hdr = reinterpret_cast<const uint4*>(a.in + 32);
+  const uint64_t* pay = reinterpret_cast<const uint64_t*>(a.in + 32 + 16 * sh.n_blocks);
+  const uint32_t nblk = (uint32_t)sh.n_blocks;
+  uint32_t err = 0;
+  for (uint32_t b = tid; b < nblk; b += NT) {
+    const uint4 h = hdr[b];
+    const uint64_t nb = min(sh.Le, sh.n - (uint64_t)b * sh.Le);
+    const uint32_t k = (h.x == CODEC_BASIC && h.z != 0) ? capacity_of((uint64_t)h.z + 1) : 1u;
+    err |= check_block(h, nb, sh.width, k);
+    s_nw[b] = h.w;
+  }
+  __syncthreads();
+  const uint64_t total = cta_exclusive_scan<uint64_t>(s_nw, s_off, nblk, s_warp);
+  if (blockIdx.x == 0 && tid == 0 && total != payload_words) err |= POLY_ST_LENGTH;
+  if (blockIdx.x != 0) err = 0;  // header verdicts reported once
+  V* out = reinterpret_cast<V*>(a.out);
+  for (uint64_t id = blockIdx.x; id < sh.n_chunks; id += gridDim.x) {
+    const uint64_t b = id / sh.cpb, c = id % sh.cpb;
+    const uint64_t lo = b * sh.Le, nb = min(sh.Le, sh.n - lo);
+    if (c * CH_VALUES >= nb) continue;
+    const uint4 h = hdr[b];
+    if (h.x == CODEC_CONSTANT) {
+      if (h.z != 0 || h.w != 0) continue;
+      const uint64_t f1 = min(nb, (c + 1) * CH_VALUES);
+      for (uint64_t i = c * CH_VALUES + tid; i < f1; i += NT) out[lo + i] = (V)h.y;
+      continue;
+    }
+    if (h.x != CODEC_BASIC || h.z == 0) continue;
+    const uint64_t B = (uint64_t)h.z + 1;
+    __syncthreads();
+    if (tid == 0) s_c = dec_const_of(B);
+    __syncthreads();
+    const DecConst cst = s_c;
+    const uint32_t k = dc_k(cst);
+    if (check_block(h, nb, sh.width, k)) continue;
+    const uint64_t nw = h.w;
+    const uint64_t j0 = (c * CH_VALUES + k - 1) / k;
+    const uint64_t j1 = min(nw, ((c + 1) * CH_VALUES + k - 1) / k);
+    if (j0 >= j1) continue;
+    const uint64_t w0 = s_off[b] + j0;
+    const uint32_t cnt = (uint32_t)(j1 - j0);
+    if (w0 + cnt > payload_words) continue;  // flagged as LENGTH above
+    for (uint32_t i = tid; i < cnt; i += NT) s_words[i] = ldg_nc_u64(pay + w0 + i);
+    __syncthreads();
+    const uint64_t f0 = j0 * k;
+    uint32_t e = 0;
+    for (uint32_t i = tid; i < cnt; i += NT) {
+      const uint64_t first = (j0 + i) * k;
+      e |= decode_any<V>(s_words[i], cst, h.z, (uint32_t)min((uint64_t)k, nb - first), h.y, s_out + (first - f0));
+    }
+    err |= e;
+    __syncthreads();
+    store_values<V>(out + lo + f0, s_out, (uint32_t)(min(nb, j1 * k) - f0));
+  }
+  if (err) atomicOr(&s_err, err);
+  __syncthreads();
+  if (tid == 0 && s_err) atomicOr(a.status_out, s_err);
+}
+
 }  // namespace polyk

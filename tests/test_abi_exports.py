@@ -60,8 +60,12 @@ def test_workspace_bytes_positive(lib):
 
 def test_launches_per_call(lib):
     assert polycomp.poly_launches_per_call(556500000, 16, 30, False) == 1
-    assert polycomp.poly_launches_per_call(1 << 20, 16, 0, False) == 3
-    assert polycomp.poly_launches_per_call(1 << 20, 16, 0, True) == 2
+    # cfg1 (one 2 MiB block): one launch each way (poly_*_large1)
+    assert polycomp.poly_launches_per_call(1 << 20, 16, 0, False) == 1
+    assert polycomp.poly_launches_per_call(1 << 20, 16, 0, True) == 1
+    # many huge blocks keep the multi-kernel large-block path
+    assert polycomp.poly_launches_per_call(1 << 32, 16, 1 << 22, False) == 3
+    assert polycomp.poly_launches_per_call(1 << 32, 16, 1 << 22, True) == 2
 
 
 def test_argument_errors_without_launch(lib):
