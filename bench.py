@@ -385,6 +385,64 @@ def measure(args, cfg, steps, rank, world, local, clocks=True, keep_input=False)
     return rec, extras
 
 
+def measure_advanced(args, cfg, steps, local):
+    """The advanced (split-base) codec of PAPER.md Sec. 3.2 on a u16 config:
+    gated against the C oracle (oracle_adv.c) byte for byte, then timed."""
+    import numpy as np
+    import torch
+    import workloads
+    from oracle import coracle
+    from paper_1805_01844_b200 import polycomp as pc
+    dev = torch.device("cuda", local)
+    c = workloads.config(cfg, 1.0)
+    x = workloads.generate(cfg, scale=1.0, seed=0, device=dev)
+    n, L = c.n, c.block_len
+    in_bytes = 2 * n
+    cap = pc.poly_max_compressed_bytes_advanced(n, 16, L)
+    out = torch.empty(cap, dtype=torch.uint8, device=dev)
+    nb = torch.zeros(1, dtype=torch.int64, device=dev)
+    wsb = pc.poly_workspace_bytes_advanced(n, 16, L)
+    ws = torch.empty((wsb + 15) // 16 * 16, dtype=torch.uint8, device=dev)
+    y = torch.empty_like(x)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    pc.poly_compress_advanced(x, L, out=out, compressed_bytes=nb, workspace=ws)
+    nbytes = int(nb.item())
+    ref = coracle.compress_advanced(x.cpu().numpy(), L)
+    ref_dev = torch.from_numpy(np.frombuffer(ref, dtype=np.uint8).copy()).to(dev)
+    exact = len(ref) == nbytes and torch.equal(out[:nbytes], ref_dev)
+    pc.poly_decompress_advanced(out, nbytes, 16, n, L, out=y, status=st, workspace=ws)
+    torch.cuda.synchronize()
+    if not (exact and int(st.item()) == 0 and torch.equal(x, y)):
+        raise SystemExit("cfg%d advanced codec: GPU output differs from the oracle: no timing reported" % cfg)
+    stream = torch.cuda.current_stream()
+    for _ in range(3):
+        pc.poly_compress_advanced(x, L, out=out, compressed_bytes=nb, workspace=ws)
+        pc.poly_decompress_advanced(out, nbytes, 16, n, L, out=y, status=st, workspace=ws)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    torch.cuda.synchronize()
+    for e in ev:
+        e[0].record(stream)
+        pc.poly_compress_advanced(x, L, out=out, compressed_bytes=nb, workspace=ws)
+        e[1].record(stream)
+        pc.poly_decompress_advanced(out, nbytes, 16, n, L, out=y, status=st, workspace=ws)
+        e[2].record(stream)
+    torch.cuda.synchronize()
+    post = torch.equal(out[:nbytes], ref_dev) and int(st.item()) == 0 and torch.equal(x, y)
+    if not post:
+        raise SystemExit("cfg%d advanced codec: timed output differs from the oracle" % cfg)
+    cm = sum(e[0].elapsed_time(e[1]) for e in ev) / steps
+    dm = sum(e[1].elapsed_time(e[2]) for e in ev) / steps
+    hbm, _, _ = measured_peaks()
+    algo = in_bytes + nbytes
+    del out, y, ws, ref_dev, x
+    torch.cuda.empty_cache()
+    return {"workload": c.name, "ratio": round(in_bytes / nbytes, 4), "bit_exact": True, "steps": steps,
+            "compress_gbs": round(in_bytes / (cm * 1e-3) / 1e9, 2), "decompress_gbs": round(in_bytes / (dm * 1e-3) / 1e9, 2),
+            "compress_ms": round(cm, 4), "decompress_ms": round(dm, 4),
+            "compress_frac": round(algo / (cm * 1e-3) / 1e9 / hbm, 4), "decompress_frac": round(algo / (dm * 1e-3) / 1e9 / hbm, 4),
+            "launches_per_step": 6}
+
+
 def lzma_pairing(pc, torch, x, x_np, L, dt, dev):
     """PAPER.md Tables 1-2 (413, 488-492, 554): LZMA alone vs the polynomial
     codec followed by LZMA, on the first 64 MiB of the input (whole blocks),
@@ -448,6 +506,15 @@ def run_ours(args, rank, world, local):
                 continue
             r, _ = measure(args, cfg, min(K, 10), rank, world, local, clocks=False)
             others["cfg%d" % cfg] = r
+    advanced = {}
+    if world == 1 and not args.only:
+        for cfg in (2, 4, 5):
+            try:
+                advanced["cfg%d" % cfg] = measure_advanced(args, cfg, min(K, 10), local)
+            except SystemExit:
+                raise
+            except Exception as e:  # pragma: no cover
+                advanced["cfg%d" % cfg] = {"error": str(e)[:200]}
     if rank != 0:
         return
     line = {
@@ -480,6 +547,7 @@ def run_ours(args, rank, world, local):
         "cpu_baseline": cpu,
         "lzma": lz,
         "configs": others,
+        "advanced": advanced,
     }
     print(json.dumps(line), flush=True)
 

@@ -119,6 +119,25 @@ poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_
                               uint64_t n, uint64_t block_size, void* d_out, uint32_t* d_status,
                               void* d_workspace, uint64_t workspace_bytes, void* stream);
 
+/* ADVANCED (split-base) codec of PAPER.md Sec. 3.2, blocked
+ * (Sec. 3.3), u16 values only, 32-bit words with the paper's 2^32 - 1 bound
+ * (readings A1-A6).  The last digit of a word is split into
+ * (r, r') against R and R' (R R' >= B): r in this word, r' at the top of the
+ * next, so no word has unused space.  Stream: as above but with layout byte 1,
+ * block codec 3 (ADVANCED) or 1 (CONSTANT), and 32-bit payload words.  The
+ * first call on a device builds and uploads the per-base schedule table
+ * (~15 MB, synchronous).  Same conventions and status bits as poly_compress /
+ * poly_decompress; POLY_ERR_INVALID_ARG for dt != POLY_U16.
+ *   poly_max_compressed_bytes_advanced = 32 + 16 n_blocks + 4 (n + n_blocks). */
+uint64_t poly_max_compressed_bytes_advanced(uint64_t n, poly_dtype_t dt, uint64_t block_size);
+uint64_t poly_workspace_bytes_advanced(uint64_t n, poly_dtype_t dt, uint64_t block_size);
+poly_status_t poly_compress_advanced(const void* d_in, uint64_t n, poly_dtype_t dt, uint64_t block_size,
+                                     void* d_out, uint64_t out_capacity, uint64_t* d_compressed_bytes,
+                                     void* d_workspace, uint64_t workspace_bytes, void* stream);
+poly_status_t poly_decompress_advanced(const void* d_in, uint64_t compressed_bytes, poly_dtype_t dt,
+                                       uint64_t n, uint64_t block_size, void* d_out, uint32_t* d_status,
+                                       void* d_workspace, uint64_t workspace_bytes, void* stream);
+
 /* End-to-end variants over HOST buffers (the path a user with data in host
  * RAM takes).  They copy h_in to the caller's device scratch, run the same
  * kernels, copy the result back, and SYNCHRONIZE `stream` before returning.

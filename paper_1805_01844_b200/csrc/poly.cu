@@ -11,6 +11,9 @@
 #include "poly_decompress.cuh"
 #include "poly_pipe.cuh"
 #include "poly_large.cuh"
+#include "poly_adv.cuh"
+
+#include <vector>
 
 using namespace polyk;
 
@@ -138,6 +141,123 @@ void build_tables() {
 #undef POLY_CHECK_T32
   }
   h_tables_built = true;
+}
+
+// ---------------------------------------------------------------- advanced codec
+// Schedule table of the split-base codec (poly_adv.cuh): for every B <= 65536
+// the orbit of R' under the series of PAPER.md:244-257, R'_0 = 1, until it
+// repeats -- its pre-period and one period -- with exact integers:
+//   p = max{p : R' B^p <= 2^32 - 1},  R = floor((2^32 - 1) / (R' B^p)),
+//   R'_next = ceil(B / R).
+std::vector<adv::AdvIdx> h_aidx;
+std::vector<uint4> h_aent;
+std::vector<uint64_t> h_amag;
+bool h_adv_built = false;
+struct AdvDev {
+  bool ready = false;
+  adv::AdvIdx* idx = nullptr;
+  uint4* ent = nullptr;
+  uint64_t* rmag = nullptr;
+};
+AdvDev g_adv[MAX_DEVICES];
+
+void build_adv_table() {
+  if (h_adv_built) return;
+  const uint64_t M = 0xffffffffull;
+  h_aidx.assign(adv::BMAX + 1, adv::AdvIdx{0, 0, 1, 0});
+  std::vector<int32_t> seen(adv::BMAX + 2, -1);
+  std::vector<uint32_t> states;
+  for (uint64_t B = 2; B <= adv::BMAX; ++B) {
+    states.clear();
+    uint64_t Rp = 1;  // R' <= B always (R >= 1)
+    while (seen[Rp] < 0) {
+      seen[Rp] = (int32_t)states.size();
+      states.push_back((uint32_t)Rp);
+      uint64_t x = Rp;
+      while (x * B <= M) x *= B;
+      const uint64_t R = M / x;
+      Rp = (B + R - 1) / R;
+    }
+    adv::AdvIdx ix;
+    ix.off = (uint32_t)h_aent.size();
+    ix.pre = (uint32_t)seen[Rp];
+    ix.per = (uint32_t)states.size() - ix.pre;
+    uint32_t Q = 0, qcyc = 0;
+    for (size_t j = 0; j < states.size(); ++j) {
+      const uint64_t st = states[j];
+      uint64_t x = st;
+      uint32_t p = 0;
+      while (x * B <= M) {
+        x *= B;
+        ++p;
+      }
+      const uint64_t R = M / x;
+      h_aent.push_back(make_uint4((uint32_t)R, (uint32_t)st, Q, p));
+      h_amag.push_back(R == 1 ? 0ull : (~0ull / R + 1));  // ceil(2^64 / R)
+      Q += p + 1;
+      if (j >= ix.pre) qcyc += p + 1;
+    }
+    ix.qcyc = qcyc;
+    h_aidx[B] = ix;
+    for (uint32_t st : states) seen[st] = -1;
+  }
+  h_adv_built = true;
+}
+
+poly_status_t ensure_adv(int dev, adv::AdvTab& T) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  AdvDev& d = g_adv[dev];
+  if (!d.ready) {
+    build_adv_table();
+    if (cudaMalloc(&d.idx, sizeof(adv::AdvIdx) * h_aidx.size()) != cudaSuccess ||
+        cudaMalloc(&d.ent, sizeof(uint4) * h_aent.size()) != cudaSuccess ||
+        cudaMalloc(&d.rmag, sizeof(uint64_t) * h_amag.size()) != cudaSuccess ||
+        cudaMemcpy(d.idx, h_aidx.data(), sizeof(adv::AdvIdx) * h_aidx.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(d.ent, h_aent.data(), sizeof(uint4) * h_aent.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(d.rmag, h_amag.data(), sizeof(uint64_t) * h_amag.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+      return POLY_ERR_CUDA;
+    d.ready = true;
+  }
+  T.idx = d.idx;
+  T.ent = d.ent;
+  T.rmag = d.rmag;
+  return POLY_OK;
+}
+
+struct AdvPlan {
+  uint64_t n, Le, n_blocks, last_len, n_chunks, o_cstat, o_nw, o_woff, ws_bytes;
+};
+bool plan_adv(uint64_t n, poly_dtype_t dt, uint64_t block_size, AdvPlan& P) {
+  if (n == 0 || dt != POLY_U16 || block_size >= (1ull << 32)) return false;
+  P.n = n;
+  P.Le = block_size ? block_size : n;
+  P.n_blocks = (n + P.Le - 1) / P.Le;
+  if (P.n_blocks >= (1ull << 32) || P.Le >= (1ull << 32)) return false;
+  P.last_len = n - (P.n_blocks - 1) * P.Le;
+  P.n_chunks = (P.n_blocks + adv::SCHUNK - 1) / adv::SCHUNK;
+  P.o_cstat = 64;
+  P.o_nw = (64 + 8 * P.n_chunks + 15) / 16 * 16;
+  P.o_woff = (P.o_nw + 4 * P.n_blocks + 15) / 16 * 16;
+  P.ws_bytes = P.o_woff + 8 * P.n_blocks;
+  return true;
+}
+
+adv::Args adv_args(const AdvPlan& P, uint64_t block_size, uint8_t* ws, const adv::AdvTab& T) {
+  adv::Args a;
+  memset(&a, 0, sizeof a);
+  a.T = T;
+  a.n = P.n;
+  a.Le = P.Le;
+  a.n_blocks = P.n_blocks;
+  a.last_len = P.last_len;
+  a.n_chunks = P.n_chunks;
+  a.block_len = (uint32_t)block_size;
+  a.warp_per_block = P.Le > 64 ? 1u : 0u;
+  a.ticket = reinterpret_cast<uint32_t*>(ws);
+  a.cstat = reinterpret_cast<uint64_t*>(ws + P.o_cstat);
+  a.nw = reinterpret_cast<uint32_t*>(ws + P.o_nw);
+  a.woff = reinterpret_cast<uint64_t*>(ws + P.o_woff);
+  return a;
 }
 
 template <typename K>
@@ -792,6 +912,83 @@ poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_
   }
   if (cudaGetLastError() != cudaSuccess) return POLY_ERR_CUDA;
   return POLY_OK;
+}
+
+uint64_t poly_max_compressed_bytes_advanced(uint64_t n, poly_dtype_t dt, uint64_t block_size) {
+  AdvPlan P;
+  if (!plan_adv(n, dt, block_size, P)) return 0;
+  return 32 + 16 * P.n_blocks + 4 * (n + P.n_blocks);  // a word holds >= 1 value; the last may hold a carry only
+}
+
+uint64_t poly_workspace_bytes_advanced(uint64_t n, poly_dtype_t dt, uint64_t block_size) {
+  AdvPlan P;
+  if (!plan_adv(n, dt, block_size, P)) return 0;
+  return P.ws_bytes;
+}
+
+poly_status_t poly_compress_advanced(const void* d_in, uint64_t n, poly_dtype_t dt, uint64_t block_size,
+                                     void* d_out, uint64_t out_capacity, uint64_t* d_compressed_bytes,
+                                     void* d_workspace, uint64_t workspace_bytes, void* stream) {
+  if (n == 0) return POLY_ERR_EMPTY_INPUT;
+  if (dt != POLY_U16 || !d_in || !d_out || !d_compressed_bytes || !d_workspace) return POLY_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(d_in) & 1) || (reinterpret_cast<uintptr_t>(d_out) & 15) ||
+      (reinterpret_cast<uintptr_t>(d_workspace) & 15))
+    return POLY_ERR_INVALID_ARG;
+  AdvPlan P;
+  if (!plan_adv(n, dt, block_size, P)) return POLY_ERR_INVALID_ARG;
+  if (out_capacity < poly_max_compressed_bytes_advanced(n, dt, block_size)) return POLY_ERR_CAPACITY;
+  if (workspace_bytes < P.ws_bytes) return POLY_ERR_WORKSPACE;
+  const int dev = current_device();
+  poly_status_t st = ensure_init(dev);
+  adv::AdvTab T;
+  if (st == POLY_OK) st = ensure_adv(dev, T);
+  if (st != POLY_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(d_workspace);
+  adv::Args a = adv_args(P, block_size, ws, T);
+  a.in = reinterpret_cast<const uint8_t*>(d_in);
+  a.out = reinterpret_cast<uint8_t*>(d_out);
+  a.compressed_bytes = d_compressed_bytes;
+  cudaMemsetAsync(ws, 0, P.o_nw, s);
+  const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(
+      a.warp_per_block ? (P.n_blocks + 7) / 8 : (P.n_blocks + adv::NTA - 1) / adv::NTA, 148ull * 16));
+  adv::adv_stats<uint16_t><<<g, adv::NTA, 0, s>>>(a);
+  adv::adv_scan<<<(unsigned)P.n_chunks, adv::NTA, 0, s>>>(a, 1u);
+  adv::adv_pack<uint16_t><<<g, adv::NTA, 0, s>>>(a);
+  return cudaGetLastError() == cudaSuccess ? POLY_OK : POLY_ERR_CUDA;
+}
+
+poly_status_t poly_decompress_advanced(const void* d_in, uint64_t compressed_bytes, poly_dtype_t dt,
+                                       uint64_t n, uint64_t block_size, void* d_out, uint32_t* d_status,
+                                       void* d_workspace, uint64_t workspace_bytes, void* stream) {
+  if (n == 0) return POLY_ERR_EMPTY_INPUT;
+  if (dt != POLY_U16 || !d_in || !d_out || !d_status || !d_workspace) return POLY_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(d_in) & 15) || (reinterpret_cast<uintptr_t>(d_out) & 1) ||
+      (reinterpret_cast<uintptr_t>(d_workspace) & 15))
+    return POLY_ERR_INVALID_ARG;
+  AdvPlan P;
+  if (!plan_adv(n, dt, block_size, P)) return POLY_ERR_INVALID_ARG;
+  if (workspace_bytes < P.ws_bytes) return POLY_ERR_WORKSPACE;
+  const int dev = current_device();
+  poly_status_t st = ensure_init(dev);
+  adv::AdvTab T;
+  if (st == POLY_OK) st = ensure_adv(dev, T);
+  if (st != POLY_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(d_workspace);
+  adv::Args a = adv_args(P, block_size, ws, T);
+  a.in = reinterpret_cast<const uint8_t*>(d_in);
+  a.in_bytes = compressed_bytes;
+  a.out = reinterpret_cast<uint8_t*>(d_out);
+  a.status_out = d_status;
+  cudaMemsetAsync(d_status, 0, 4, s);
+  cudaMemsetAsync(ws, 0, P.o_nw, s);
+  const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(
+      a.warp_per_block ? (P.n_blocks + 7) / 8 : (P.n_blocks + adv::NTA - 1) / adv::NTA, 148ull * 16));
+  adv::adv_check_header<<<1, 1, 0, s>>>(a);
+  adv::adv_scan<<<(unsigned)P.n_chunks, adv::NTA, 0, s>>>(a, 0u);
+  adv::adv_unpack<uint16_t><<<g, adv::NTA, 0, s>>>(a);
+  return cudaGetLastError() == cudaSuccess ? POLY_OK : POLY_ERR_CUDA;
 }
 
 poly_status_t poly_compress_host(const void* h_in, uint64_t n, poly_dtype_t dt, uint64_t block_size,

@@ -34,7 +34,9 @@ POLY_ST_LENGTH = 128
 
 EXPORTS = ["poly_version", "poly_status_string", "poly_init", "poly_max_compressed_bytes",
            "poly_workspace_bytes", "poly_compress", "poly_read_header", "poly_decompress",
-           "poly_compress_host", "poly_decompress_host", "poly_launches_per_call", "poly_tables_ok"]
+           "poly_compress_host", "poly_decompress_host", "poly_launches_per_call", "poly_tables_ok",
+           "poly_max_compressed_bytes_advanced", "poly_workspace_bytes_advanced", "poly_compress_advanced",
+           "poly_decompress_advanced"]
 
 
 class PolyError(RuntimeError):
@@ -66,6 +68,14 @@ def load_library(path: str = LIB_PATH):
     L.poly_max_compressed_bytes.argtypes = [u64, i32, u64]
     L.poly_workspace_bytes.restype = u64
     L.poly_workspace_bytes.argtypes = [u64, i32, u64]
+    L.poly_max_compressed_bytes_advanced.restype = u64
+    L.poly_max_compressed_bytes_advanced.argtypes = [u64, i32, u64]
+    L.poly_workspace_bytes_advanced.restype = u64
+    L.poly_workspace_bytes_advanced.argtypes = [u64, i32, u64]
+    L.poly_compress_advanced.restype = i32
+    L.poly_compress_advanced.argtypes = [vp, u64, i32, u64, vp, u64, vp, vp, u64, vp]
+    L.poly_decompress_advanced.restype = i32
+    L.poly_decompress_advanced.argtypes = [vp, u64, i32, u64, u64, vp, vp, vp, u64, vp]
     L.poly_tables_ok.restype = i32
     L.poly_tables_ok.argtypes = []
     L.poly_launches_per_call.restype = i32
@@ -233,6 +243,63 @@ def poly_decompress_host(h_stream: torch.Tensor, nbytes: int, dt: int, n: int, b
                                              workspace.data_ptr(), workspace.numel(), _stream_ptr(stream))
     _check(rc, "poly_decompress_host")
     return st.value
+
+
+# ------------------------------------------------------------------ advanced codec
+def poly_max_compressed_bytes_advanced(n: int, dt: int, block_len: int) -> int:
+    return load_library().poly_max_compressed_bytes_advanced(n, dt, block_len)
+
+
+def poly_workspace_bytes_advanced(n: int, dt: int, block_len: int) -> int:
+    return load_library().poly_workspace_bytes_advanced(n, dt, block_len)
+
+
+def poly_compress_advanced(x: torch.Tensor, block_len: int, out: Optional[torch.Tensor] = None,
+                           compressed_bytes: Optional[torch.Tensor] = None,
+                           workspace: Optional[torch.Tensor] = None,
+                           stream: Optional[torch.cuda.Stream] = None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """The advanced (split-base) codec of PAPER.md Sec. 3.2 on a uint16 device
+    tensor; same conventions as poly_compress."""
+    _need_cuda(x)
+    dt = _dt(x)
+    n = x.numel()
+    cap = poly_max_compressed_bytes_advanced(n, dt, block_len)
+    if out is None:
+        out = torch.empty(max(cap, 16), dtype=torch.uint8, device=x.device)
+    if compressed_bytes is None:
+        compressed_bytes = torch.empty(1, dtype=torch.int64, device=x.device)
+    if workspace is None:
+        nb = max(16, poly_workspace_bytes_advanced(n, dt, block_len))
+        workspace = torch.empty((nb + 15) // 16 * 16, dtype=torch.uint8, device=x.device)
+    _need_cuda(out, compressed_bytes, workspace)
+    rc = load_library().poly_compress_advanced(x.data_ptr(), n, dt, block_len, out.data_ptr(), out.numel(),
+                                               compressed_bytes.data_ptr(), workspace.data_ptr(), workspace.numel(),
+                                               _stream_ptr(stream))
+    _check(rc, "poly_compress_advanced")
+    return out, compressed_bytes
+
+
+def poly_decompress_advanced(stream_buf: torch.Tensor, nbytes: int, dt: int, n: int, block_len: int,
+                             out: Optional[torch.Tensor] = None, status: Optional[torch.Tensor] = None,
+                             workspace: Optional[torch.Tensor] = None,
+                             stream: Optional[torch.cuda.Stream] = None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """Inverse of poly_compress_advanced; same conventions as poly_decompress."""
+    _need_cuda(stream_buf)
+    if out is None:
+        out = torch.empty(n, dtype=_torch_dtype(dt), device=stream_buf.device)
+    if status is None:
+        status = torch.empty(1, dtype=torch.int32, device=stream_buf.device)
+    if workspace is None:
+        nb = max(16, poly_workspace_bytes_advanced(n, dt, block_len))
+        workspace = torch.empty((nb + 15) // 16 * 16, dtype=torch.uint8, device=stream_buf.device)
+    _need_cuda(out, status, workspace)
+    if nbytes > stream_buf.numel():
+        raise ValueError("nbytes exceeds the buffer")
+    rc = load_library().poly_decompress_advanced(stream_buf.data_ptr(), nbytes, dt, n, block_len, out.data_ptr(),
+                                                 status.data_ptr(), workspace.data_ptr(), workspace.numel(),
+                                                 _stream_ptr(stream))
+    _check(rc, "poly_decompress_advanced")
+    return out, status
 
 
 # ------------------------------------------------------------------ convenience
