@@ -52,7 +52,7 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=100)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
+    p.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5, 6])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -501,7 +501,7 @@ def run_ours(args, rank, world, local):
     torch.cuda.empty_cache()
     others = {}
     if world == 1 and not args.only:
-        for cfg in (1, 2, 3, 4, 5):
+        for cfg in (1, 2, 3, 4, 5, 6):  # 6: cfg2 in the paper's time-major layout
             if cfg == args.config:
                 continue
             r, _ = measure(args, cfg, min(K, 10), rank, world, local, clocks=False)

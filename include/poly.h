@@ -20,8 +20,11 @@
  *     Device-side calls are asynchronous on `stream`; they never allocate,
  *     free or synchronize, and keep no pointer after they return.  The caller
  *     owns every buffer.
- *   - Arrays of values are little-endian u16 (POLY_U16) or u32 (POLY_U32),
- *     contiguous, with no alignment requirement (16-byte alignment is faster).
+ *   - Arrays of values are u8 (POLY_U8), little-endian u16
+ *     (POLY_U16) or u32 (POLY_U32), contiguous, aligned to their element size
+ *     only (16-byte alignment is faster).  A compressed stream buffer (the
+ *     output of poly_compress, the input of poly_decompress) must be 16-byte
+ *     aligned (POLY_ERR_INVALID_ARG otherwise; torch / cudaMalloc buffers are).
  *   - Argument errors are returned synchronously, with nothing launched.
  *     Errors in stream CONTENT are only known on the device and are reported
  *     as POLY_ST_* bits in the caller's device status word.
@@ -38,7 +41,7 @@
 extern "C" {
 #endif
 
-typedef enum { POLY_U16 = 16, POLY_U32 = 32 } poly_dtype_t;
+typedef enum { POLY_U8 = 8, POLY_U16 = 16, POLY_U32 = 32 } poly_dtype_t;
 
 typedef enum {
   POLY_OK = 0,
@@ -80,8 +83,8 @@ const char* poly_status_string(poly_status_t s);
 poly_status_t poly_init(int device);
 
 /* Worst-case stream size for n values of dtype `dt` in blocks of block_size:
- * 32 + 16 n_blocks + 8 sum_b ceil(n_b / k_min), k_min = 4 (u16), 2 (u32)
- * (the smallest k under R2 for B <= 2^16 resp. 2^32).  0 if n == 0. */
+ * 32 + 16 n_blocks + 8 sum_b ceil(n_b / k_min), k_min = 8 (u8), 4 (u16), 2 (u32)
+ * (the smallest k under R2 for B <= 2^8, 2^16 resp. 2^32).  0 if n == 0. */
 uint64_t poly_max_compressed_bytes(uint64_t n, poly_dtype_t dt, uint64_t block_size);
 
 /* Device workspace bytes needed by poly_compress / poly_decompress and the

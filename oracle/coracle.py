@@ -83,12 +83,9 @@ def capacity(B: int) -> int:
 def compress(x: np.ndarray, block_len: int, threads: int | None = None) -> bytes:
     """x: contiguous uint16 or uint32 numpy array.  Returns the stream bytes."""
     x = np.ascontiguousarray(x)
-    if x.dtype == np.uint16:
-        w = 16
-    elif x.dtype == np.uint32:
-        w = 32
-    else:
-        raise TypeError("uint16 or uint32 only")
+    w = {np.dtype(np.uint8): 8, np.dtype(np.uint16): 16, np.dtype(np.uint32): 32}.get(x.dtype)
+    if w is None:
+        raise TypeError("uint8, uint16 or uint32 only")
     n = x.size
     cap = lib().oracle_max_compressed_bytes(n, w, block_len)
     out = np.empty(cap, dtype=np.uint8)
@@ -112,7 +109,7 @@ def decompress(stream: bytes | np.ndarray, threads: int | None = None) -> Tuple[
     else:
         n, w = 0, 16
     cap = n if n < (1 << 36) else 0
-    out = np.empty(max(cap, 1), dtype=np.uint32 if w == 32 else np.uint16)
+    out = np.empty(max(cap, 1), dtype={8: np.uint8, 32: np.uint32}.get(w, np.uint16))
     n_out = ctypes.c_uint64(0)
     w_out = ctypes.c_int(0)
     st = ctypes.c_uint32(0)

@@ -53,12 +53,14 @@ int oracle_capacity(uint64_t B) {
 }
 
 static uint64_t get_value(const void* in, int width_bits, uint64_t i) {
+    if (width_bits == 8) return ((const uint8_t*)in)[i];
     if (width_bits == 16) return ((const uint16_t*)in)[i];
     return ((const uint32_t*)in)[i];
 }
 
 static void put_value(void* out, int width_bits, uint64_t i, uint64_t v) {
-    if (width_bits == 16) ((uint16_t*)out)[i] = (uint16_t)v;
+    if (width_bits == 8) ((uint8_t*)out)[i] = (uint8_t)v;
+    else if (width_bits == 16) ((uint16_t*)out)[i] = (uint16_t)v;
     else ((uint32_t*)out)[i] = (uint32_t)v;
 }
 
@@ -84,7 +86,8 @@ uint64_t oracle_max_compressed_bytes(uint64_t n, int width_bits, uint64_t block_
     uint64_t L = block_len == 0 ? n : block_len;
     uint64_t nb = (n + L - 1) / L;
     /* smallest k: u16 -> 4 (B <= 2^16), u32 -> 2 (B <= 2^32) */
-    uint64_t kmin = width_bits == 16 ? 4 : 2;
+    /* smallest k: u8 -> 8 (B <= 2^8), u16 -> 4 (B <= 2^16), u32 -> 2 (B <= 2^32) */
+    uint64_t kmin = width_bits == 8 ? 8 : (width_bits == 16 ? 4 : 2);
     uint64_t words = 0;
     uint64_t full = n / L, last = n - full * L;
     words += full * ((L + kmin - 1) / kmin);
@@ -181,7 +184,7 @@ static void run_jobs(cjob_t* base, int threads, void* (*fn)(void*)) {
 int oracle_compress(const void* in, uint64_t n, int width_bits, uint64_t block_len,
                     uint8_t* out, uint64_t out_capacity, uint64_t* out_bytes, int threads) {
     if (n == 0) return 1;
-    if (width_bits != 16 && width_bits != 32) return 2;
+    if (width_bits != 8 && width_bits != 16 && width_bits != 32) return 2;
     if (block_len >= (1ull << 32)) return 2;
     uint64_t L = block_len == 0 ? n : block_len;
     uint64_t n_blocks = (n + L - 1) / L;
@@ -272,7 +275,7 @@ int oracle_decompress(const uint8_t* in, uint64_t in_bytes, void* out, uint64_t 
     if (!(in[0] == 'P' && in[1] == 'L' && in[2] == 'Y' && in[3] == 'C')) { *status = OST_BAD_MAGIC; return 1; }
     if (in[4] != 2) { *status = OST_BAD_VERSION; return 1; }
     int width_bits = in[6];
-    if (in[5] != 0 || in[7] != 0 || (width_bits != 16 && width_bits != 32)) { *status = OST_HEADER_MISMATCH; return 1; }
+    if (in[5] != 0 || in[7] != 0 || (width_bits != 8 && width_bits != 16 && width_bits != 32)) { *status = OST_HEADER_MISMATCH; return 1; }
     uint64_t n = get_u64(in + 8);
     uint64_t block_len = get_u32(in + 16);
     uint64_t n_blocks = get_u32(in + 20);

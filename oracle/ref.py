@@ -215,8 +215,8 @@ def compress_blocked(values: Sequence[int], width_bits: int, block_len: int) -> 
     n = len(values)
     if n == 0:
         raise EmptyInput("compress of an empty vector")
-    if width_bits not in (16, 32):
-        raise ValueError("width_bits must be 16 or 32")
+    if width_bits not in (8, 16, 32):       # SPEC.md:30 widths
+        raise ValueError("width_bits must be 8, 16 or 32")
     for v in values:
         if not (0 <= v < (1 << width_bits)):
             raise ValueError("value does not fit the declared width")
@@ -238,7 +238,7 @@ def parse_header(stream: bytes) -> Tuple[int, int, int, int, int]:
     version, layout, width_bits, policy = struct.unpack_from("<BBBB", stream, 4)
     if version != VERSION:
         raise UnsupportedVersion("version %d" % version)
-    if layout != 0 or policy != 0 or width_bits not in (16, 32):
+    if layout != 0 or policy != 0 or width_bits not in (8, 16, 32):
         raise CorruptStream("bad layout/policy/width")
     (n,) = struct.unpack_from("<Q", stream, 8)
     block_len, n_blocks = struct.unpack_from("<II", stream, 16)

@@ -17,6 +17,27 @@
 
 using namespace polyk;
 
+// Value type of a dtype, for the kernel templates: runs BODY with V bound.
+#define POLY_DISPATCH(dt, ...)         \
+  do {                                 \
+    if ((dt) == POLY_U8) {             \
+      typedef uint8_t V;               \
+      __VA_ARGS__;                     \
+    } else if ((dt) == POLY_U16) {     \
+      typedef uint16_t V;              \
+      __VA_ARGS__;                     \
+    } else {                           \
+      typedef uint32_t V;              \
+      __VA_ARGS__;                     \
+    }                                  \
+  } while (0)
+
+namespace {
+// Smallest capacity k of any base of a width (B <= 2^w): u8 8, u16 4, u32 2.
+inline uint64_t kmin_of(uint32_t w) { return w == 8 ? 8 : (w == 16 ? 4 : 2); }
+inline bool dt_ok(poly_dtype_t dt) { return dt == POLY_U8 || dt == POLY_U16 || dt == POLY_U32; }
+}  // namespace
+
 namespace {
 // Consumer warps of the pipeline kernels (compress / decompress).
 // (measured on cfg2/4/5: more warps hide the lane-per-block latency of map 0
@@ -272,6 +293,21 @@ uint32_t large_smem_unpack() {
   return 16 * ((CH_VALUES + 64) * sizeof(V) / 16 + 1) + 8 * (CH_VALUES / 2 + 2);
 }
 
+template <typename V>
+void set_attrs(int pmax) {
+  set_smem_attr(poly_compress_pipe<V, 0, NCW_C>, pmax);
+  set_smem_attr(poly_compress_pipe<V, 1, NCW_C>, pmax);
+  set_smem_attr(poly_decompress_pipe<V, 0, NCW_D0>, pmax);
+  set_smem_attr(poly_decompress_pipe<V, 1, NCW_D1>, pmax);
+  set_smem_attr(poly_decompress_pipe<V, 1, NCW_D1B>, pmax);
+  set_smem_attr(poly_compress_large<V>, pmax);
+  set_smem_attr(poly_decompress_large<V>, pmax);
+  set_smem_attr(poly_compress_pack<V>, large_smem_pack<V>());
+  set_smem_attr(poly_decompress_unpack<V>, large_smem_unpack<V>());
+  set_smem_attr(poly_decompress_large1<V>, large_smem_unpack<V>());
+  set_smem_attr(poly_compress_large1<V>, large_smem_pack<V>());
+}
+
 poly_status_t ensure_init(int dev) {
   if (dev < 0 || dev >= MAX_DEVICES) return POLY_ERR_INVALID_ARG;
   std::lock_guard<std::mutex> lk(g_mu);
@@ -285,28 +321,9 @@ poly_status_t ensure_init(int dev) {
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_dtab, h_dtab, sizeof h_dtab);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
   const int pmax = (POLY_CTAS == 1 ? 227 : 113) * 1024;
-  set_smem_attr(poly_compress_pipe<uint16_t, 0, NCW_C>, pmax);
-  set_smem_attr(poly_compress_pipe<uint16_t, 1, NCW_C>, pmax);
-  set_smem_attr(poly_compress_pipe<uint32_t, 0, NCW_C>, pmax);
-  set_smem_attr(poly_compress_pipe<uint32_t, 1, NCW_C>, pmax);
-  set_smem_attr(poly_decompress_pipe<uint16_t, 0, NCW_D0>, pmax);
-  set_smem_attr(poly_decompress_pipe<uint16_t, 1, NCW_D1>, pmax);
-  set_smem_attr(poly_decompress_pipe<uint16_t, 1, NCW_D1B>, pmax);
-  set_smem_attr(poly_decompress_pipe<uint32_t, 1, NCW_D1B>, pmax);
-  set_smem_attr(poly_decompress_pipe<uint32_t, 0, NCW_D0>, pmax);
-  set_smem_attr(poly_decompress_pipe<uint32_t, 1, NCW_D1>, pmax);
-  set_smem_attr(poly_compress_large<uint16_t>, pmax);
-  set_smem_attr(poly_compress_large<uint32_t>, pmax);
-  set_smem_attr(poly_decompress_large<uint16_t>, pmax);
-  set_smem_attr(poly_decompress_large<uint32_t>, pmax);
-  set_smem_attr(poly_compress_pack<uint16_t>, large_smem_pack<uint16_t>());
-  set_smem_attr(poly_compress_pack<uint32_t>, large_smem_pack<uint32_t>());
-  set_smem_attr(poly_decompress_unpack<uint16_t>, large_smem_unpack<uint16_t>());
-  set_smem_attr(poly_decompress_large1<uint16_t>, large_smem_unpack<uint16_t>());
-  set_smem_attr(poly_decompress_large1<uint32_t>, large_smem_unpack<uint32_t>());
-  set_smem_attr(poly_compress_large1<uint16_t>, large_smem_pack<uint16_t>());
-  set_smem_attr(poly_compress_large1<uint32_t>, large_smem_pack<uint32_t>());
-  set_smem_attr(poly_decompress_unpack<uint32_t>, large_smem_unpack<uint32_t>());
+  set_attrs<uint8_t>(pmax);
+  set_attrs<uint16_t>(pmax);
+  set_attrs<uint32_t>(pmax);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (cur != dev) cudaSetDevice(cur);
   if (e != cudaSuccess) return POLY_ERR_CUDA;
@@ -335,7 +352,7 @@ bool plan_pipe_n(const Shape& sh, PipeShape& ps, bool decomp, uint32_t ncw) {
   ps.width = sh.width;
   ps.vb = sh.width / 8;
   const uint64_t bb = sh.Le * ps.vb;
-  const uint64_t kmin = sh.width == 16 ? 4 : 2;
+  const uint64_t kmin = kmin_of(sh.width);
   if (bb <= MAP0_MAX_BLOCK) {
     ps.map = 0;
     uint64_t bpt = PIPE_TILE_TARGET / (pc * bb);
@@ -450,7 +467,7 @@ bool plan_large(const Shape& sh, LargeShape& ls, bool decomp) {
     ls.o_in = ctl;
     ls.smem = ctl + ls.S * ls.stage;
   } else {
-    const uint64_t kmin = sh.width == 16 ? 4 : 2;
+    const uint64_t kmin = kmin_of(sh.width);
     ls.stage = r16(8ull * (ls.SV / kmin + 4));
     const uint32_t outb = 2 * ls.SV * ls.vb;
     ls.S = (uint32_t)std::min<uint64_t>(MAXS, (PIPE_SMEM_MAX - ctl - outb) / ls.stage);
@@ -463,7 +480,7 @@ bool plan_large(const Shape& sh, LargeShape& ls, bool decomp) {
 }
 
 bool plan(uint64_t n, uint32_t w, uint64_t block_size, Shape& sh, Regime& rg) {
-  if (n == 0 || (w != 16 && w != 32) || block_size >= (1ull << 32)) return false;
+  if (n == 0 || (w != 8 && w != 16 && w != 32) || block_size >= (1ull << 32)) return false;
   memset(&sh, 0, sizeof sh);
   sh.n = n;
   sh.width = w;
@@ -473,7 +490,7 @@ bool plan(uint64_t n, uint32_t w, uint64_t block_size, Shape& sh, Regime& rg) {
   if (sh.n_blocks >= (1ull << 32)) return false;
   // a block header holds n_words in 32 bits: ceil(L_e / k_min) < 2^32 (only a
   // block_size = 0 call with n >= 2^33 (u32) / 2^34 (u16) exceeds it)
-  if ((sh.Le + (w == 16 ? 3 : 1)) / (w == 16 ? 4 : 2) >= (1ull << 32)) return false;
+  if ((sh.Le + kmin_of(w) - 1) / kmin_of(w) >= (1ull << 32)) return false;
   const uint64_t bb = sh.Le * (w / 8);  // bytes per block
   PipeShape pc, pd;
   LargeShape lc, ld;
@@ -605,6 +622,7 @@ void launch_compress_pipe(const Shape& sh, poly_dtype_t dt, const void* d_in, ui
   pa.status = reinterpret_cast<uint64_t*>(ws + W.status_off);
   pa.ticket = reinterpret_cast<uint32_t*>(ws);
   pa.bulk = ((reinterpret_cast<uintptr_t>(d_in) & 15) == 0 && pa.sh.tile_bytes % 16 == 0) ? 1u : 0u;
+  pa.tma_shift = ((reinterpret_cast<uintptr_t>(d_in) & 15) == 0 && pa.sh.tile_bytes % 16 != 0) ? 1u : 0u;
   pa.debug = debug_flags();
   pa.t_begin = t_begin;
   pa.t_end = std::min<uint64_t>(t_end, pa.sh.n_tiles);
@@ -612,10 +630,11 @@ void launch_compress_pipe(const Shape& sh, poly_dtype_t dt, const void* d_in, ui
   // to the writers: 4 of them keep up (measured: 2 -> 1254, 4 -> 2078 GB/s cfg2)
   const bool wr = pa.sh.wrings != 0;
   pa.nlb = lb_warps(wr ? 4 : 2, NLB_MAX + 1);
-  auto k = dt == POLY_U16 ? (pa.sh.map == 0 ? poly_compress_pipe<uint16_t, 0, NCW_C> : poly_compress_pipe<uint16_t, 1, NCW_C>)
-                          : (pa.sh.map == 0 ? poly_compress_pipe<uint32_t, 0, NCW_C> : poly_compress_pipe<uint32_t, 1, NCW_C>);
-  const int grid = pipe_grid_server(k, pipe_threads(NCW_C), pa.sh.smem, pa.t_end - pa.t_begin, dev, pa.server);
-  launch_k(k, grid, pipe_threads(NCW_C), pa.sh.smem, s, pa.server != 0, pa);
+  POLY_DISPATCH(dt, {
+    auto k = pa.sh.map == 0 ? poly_compress_pipe<V, 0, NCW_C> : poly_compress_pipe<V, 1, NCW_C>;
+    const int grid = pipe_grid_server(k, pipe_threads(NCW_C), pa.sh.smem, pa.t_end - pa.t_begin, dev, pa.server);
+    launch_k(k, grid, pipe_threads(NCW_C), pa.sh.smem, s, pa.server != 0, pa);
+  });
 }
 
 // One poly_decompress_pipe launch over tiles [t_begin, t_end) (clipped).
@@ -640,14 +659,13 @@ void launch_decompress_pipe(const Shape& sh, poly_dtype_t dt, const uint8_t* d_i
   // (map 1: the last helper warp is the tile store warp)
   // (map 1: one look-back warp, measured cfg5 1948 -> 2044 GB/s, cfg4 1390 -> 1398)
   pa.nlb = lb_warps(pa.sh.map == 1 ? 1 : 2, std::min<uint32_t>(pa.sh.map != 0 ? NLB_MAX - 1 : NLB_MAX, pa.sh.S));
-  auto k = dt == POLY_U16
-               ? (pa.sh.map == 0   ? poly_decompress_pipe<uint16_t, 0, NCW_D0>
-                  : pa.sh.ncw == NCW_D1 ? poly_decompress_pipe<uint16_t, 1, NCW_D1> : poly_decompress_pipe<uint16_t, 1, NCW_D1B>)
-               : (pa.sh.map == 0   ? poly_decompress_pipe<uint32_t, 0, NCW_D0>
-                  : pa.sh.ncw == NCW_D1 ? poly_decompress_pipe<uint32_t, 1, NCW_D1> : poly_decompress_pipe<uint32_t, 1, NCW_D1B>);
-  const int nt = pipe_threads((int)pa.sh.ncw);
-  const int grid = pipe_grid_server(k, nt, pa.sh.smem, pa.t_end - pa.t_begin, dev, pa.server);
-  launch_k(k, grid, nt, pa.sh.smem, s, pa.server != 0, pa);
+  POLY_DISPATCH(dt, {
+    auto k = pa.sh.map == 0 ? poly_decompress_pipe<V, 0, NCW_D0>
+             : pa.sh.ncw == NCW_D1 ? poly_decompress_pipe<V, 1, NCW_D1> : poly_decompress_pipe<V, 1, NCW_D1B>;
+    const int nt = pipe_threads((int)pa.sh.ncw);
+    const int grid = pipe_grid_server(k, nt, pa.sh.smem, pa.t_end - pa.t_begin, dev, pa.server);
+    launch_k(k, grid, nt, pa.sh.smem, s, pa.server != 0, pa);
+  });
 }
 
 // Streams, events and pinned prefix slots of the chunked host calls.
@@ -705,10 +723,10 @@ const char* poly_status_string(poly_status_t s) {
 poly_status_t poly_init(int device) { return ensure_init(device); }
 
 uint64_t poly_max_compressed_bytes(uint64_t n, poly_dtype_t dt, uint64_t block_size) {
-  if (n == 0 || (dt != POLY_U16 && dt != POLY_U32)) return 0;
+  if (n == 0 || !dt_ok(dt)) return 0;
   const uint64_t L = block_size == 0 ? n : block_size;
   const uint64_t nb = (n + L - 1) / L;
-  const uint64_t kmin = dt == POLY_U16 ? 4 : 2;
+  const uint64_t kmin = kmin_of((uint32_t)dt);
   const uint64_t full = n / L, last = n - full * L;
   uint64_t words = full * ((L + kmin - 1) / kmin);
   if (last) words += (last + kmin - 1) / kmin;
@@ -748,7 +766,7 @@ int poly_launches_per_call(uint64_t n, poly_dtype_t dt, uint64_t block_size, int
 poly_status_t poly_compress(const void* d_in, uint64_t n, poly_dtype_t dt, uint64_t block_size,
                             void* d_out, uint64_t out_capacity, uint64_t* d_compressed_bytes,
                             void* d_workspace, uint64_t workspace_bytes, void* stream) {
-  if (dt != POLY_U16 && dt != POLY_U32) return POLY_ERR_INVALID_ARG;
+  if (!dt_ok(dt)) return POLY_ERR_INVALID_ARG;
   if (n == 0) return POLY_ERR_EMPTY_INPUT;
   if (!d_in || !d_out || !d_compressed_bytes || !d_workspace) return POLY_ERR_INVALID_ARG;
   const uint32_t vb = (uint32_t)dt / 8;
@@ -787,9 +805,11 @@ poly_status_t poly_compress(const void* d_in, uint64_t n, poly_dtype_t dt, uint6
     la.status = a.status;
     la.ticket = a.ticket;
     la.bulk = ((reinterpret_cast<uintptr_t>(d_in) & 15) == 0 && (sh.Le * (dt / 8)) % 16 == 0) ? 1u : 0u;
-    auto k = dt == POLY_U16 ? poly_compress_large<uint16_t> : poly_compress_large<uint32_t>;
-    const int grid = pipe_grid_server(k, PT, la.sh.smem, sh.n_blocks, dev, la.server);
-    launch_k(k, grid, PT, la.sh.smem, s, la.server != 0, la);
+    POLY_DISPATCH(dt, {
+      auto k = poly_compress_large<V>;
+      const int grid = pipe_grid_server(k, PT, la.sh.smem, sh.n_blocks, dev, la.server);
+      launch_k(k, grid, PT, la.sh.smem, s, la.server != 0, la);
+    });
   } else if (rg == PIPE) {
     cudaMemsetAsync(ws, 0, W.total, s);
     launch_compress_pipe(sh, dt, d_in, a.out, d_compressed_bytes, ws, W, 0, ~0ull, s, dev);
@@ -799,25 +819,23 @@ poly_status_t poly_compress(const void* d_in, uint64_t n, poly_dtype_t dt, uint6
     a.woff = reinterpret_cast<uint64_t*>(ws + W.woff_off);
     cudaMemsetAsync(ws, 0, W.bmin_off, s);
     if (large1_compress(sh)) {  // one cooperative launch (grid barrier inside)
-      auto k = dt == POLY_U16 ? poly_compress_large1<uint16_t> : poly_compress_large1<uint32_t>;
-      const uint32_t smem = dt == POLY_U16 ? large_smem_pack<uint16_t>() : large_smem_pack<uint32_t>();
-      const int grid = pipe_grid(k, smem, sh.n_chunks, dev, NT);
-      launch_k(k, grid, NT, smem, s, true, a);
+      POLY_DISPATCH(dt, {
+        auto k = poly_compress_large1<V>;
+        const uint32_t smem = large_smem_pack<V>();
+        const int grid = pipe_grid(k, smem, sh.n_chunks, dev, NT);
+        launch_k(k, grid, NT, smem, s, true, a);
+      });
       if (cudaGetLastError() != cudaSuccess) return POLY_ERR_CUDA;
       return POLY_OK;
     }
     cudaMemsetAsync(a.bmin, 0xff, 4 * sh.n_blocks, s);
     cudaMemsetAsync(a.bmax, 0, 4 * sh.n_blocks, s);
     const int gr = grid_for(sh.n_chunks, dev);
-    if (dt == POLY_U16) {
-      poly_compress_minmax<uint16_t><<<gr, NT, 0, s>>>(a);
+    POLY_DISPATCH(dt, {
+      poly_compress_minmax<V><<<gr, NT, 0, s>>>(a);
       poly_compress_block_scan<<<(unsigned)sh.n_stiles, NT, 0, s>>>(a);
-      poly_compress_pack<uint16_t><<<gr, NT, large_smem_pack<uint16_t>(), s>>>(a);
-    } else {
-      poly_compress_minmax<uint32_t><<<gr, NT, 0, s>>>(a);
-      poly_compress_block_scan<<<(unsigned)sh.n_stiles, NT, 0, s>>>(a);
-      poly_compress_pack<uint32_t><<<gr, NT, large_smem_pack<uint32_t>(), s>>>(a);
-    }
+      poly_compress_pack<V><<<gr, NT, large_smem_pack<V>(), s>>>(a);
+    });
   }
   if (cudaGetLastError() != cudaSuccess) return POLY_ERR_CUDA;
   return POLY_OK;
@@ -827,7 +845,7 @@ poly_status_t poly_read_header(const void* h_hdr32, uint64_t* n, poly_dtype_t* d
                                uint64_t* block_size, uint64_t* n_blocks, uint64_t* payload_bytes) {
   if (!h_hdr32) return POLY_ERR_INVALID_ARG;
   const uint8_t* p = reinterpret_cast<const uint8_t*>(h_hdr32);
-  if (memcmp(p, "PLYC", 4) != 0 || p[4] != 2 || p[5] != 0 || p[7] != 0 || (p[6] != 16 && p[6] != 32))
+  if (memcmp(p, "PLYC", 4) != 0 || p[4] != 2 || p[5] != 0 || p[7] != 0 || (p[6] != 8 && p[6] != 16 && p[6] != 32))
     return POLY_ERR_CORRUPT;
   uint64_t nn, pb;
   uint32_t bl, nb;
@@ -846,7 +864,7 @@ poly_status_t poly_read_header(const void* h_hdr32, uint64_t* n, poly_dtype_t* d
 poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_dtype_t dt,
                               uint64_t n, uint64_t block_size, void* d_out, uint32_t* d_status,
                               void* d_workspace, uint64_t workspace_bytes, void* stream) {
-  if (dt != POLY_U16 && dt != POLY_U32) return POLY_ERR_INVALID_ARG;
+  if (!dt_ok(dt)) return POLY_ERR_INVALID_ARG;
   if (n == 0) return POLY_ERR_EMPTY_INPUT;
   if (!d_in || !d_out || !d_status || !d_workspace) return POLY_ERR_INVALID_ARG;
   const uint32_t vb = (uint32_t)dt / 8;
@@ -886,9 +904,11 @@ poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_
     la.status = a.status;
     la.ticket = a.ticket;
     la.bulk = ((reinterpret_cast<uintptr_t>(d_out) & 15) == 0 && (sh.Le * (dt / 8)) % 16 == 0) ? 1u : 0u;
-    auto k = dt == POLY_U16 ? poly_decompress_large<uint16_t> : poly_decompress_large<uint32_t>;
-    const int grid = pipe_grid_server(k, PT, la.sh.smem, sh.n_blocks, dev, la.server);
-    launch_k(k, grid, PT, la.sh.smem, s, la.server != 0, la);
+    POLY_DISPATCH(dt, {
+      auto k = poly_decompress_large<V>;
+      const int grid = pipe_grid_server(k, PT, la.sh.smem, sh.n_blocks, dev, la.server);
+      launch_k(k, grid, PT, la.sh.smem, s, la.server != 0, la);
+    });
   } else if (rg == PIPE) {
     cudaMemsetAsync(ws, 0, W.total, s);
     launch_decompress_pipe(sh, dt, a.in, compressed_bytes, d_out, d_status, ws, W, 0, ~0ull, s, dev);
@@ -896,19 +916,13 @@ poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_
     a.woff = reinterpret_cast<uint64_t*>(ws + W.woff_off);
     const int gr = grid_for(sh.n_chunks, dev);
     if (large1_decompress(sh)) {  // one launch: every CTA scans the few headers itself
-      if (dt == POLY_U16)
-        poly_decompress_large1<uint16_t><<<gr, NT, large_smem_unpack<uint16_t>(), s>>>(a);
-      else
-        poly_decompress_large1<uint32_t><<<gr, NT, large_smem_unpack<uint32_t>(), s>>>(a);
+      POLY_DISPATCH(dt, { poly_decompress_large1<V><<<gr, NT, large_smem_unpack<V>(), s>>>(a); });
       if (cudaGetLastError() != cudaSuccess) return POLY_ERR_CUDA;
       return POLY_OK;
     }
     cudaMemsetAsync(ws, 0, W.bmin_off, s);
     poly_decompress_block_scan<<<(unsigned)sh.n_stiles, NT, 0, s>>>(a);
-    if (dt == POLY_U16)
-      poly_decompress_unpack<uint16_t><<<gr, NT, large_smem_unpack<uint16_t>(), s>>>(a);
-    else
-      poly_decompress_unpack<uint32_t><<<gr, NT, large_smem_unpack<uint32_t>(), s>>>(a);
+    POLY_DISPATCH(dt, { poly_decompress_unpack<V><<<gr, NT, large_smem_unpack<V>(), s>>>(a); });
   }
   if (cudaGetLastError() != cudaSuccess) return POLY_ERR_CUDA;
   return POLY_OK;
@@ -996,7 +1010,7 @@ poly_status_t poly_compress_host(const void* h_in, uint64_t n, poly_dtype_t dt, 
                                  void* d_in_scratch, void* d_out_scratch, uint64_t d_out_capacity,
                                  void* d_workspace, uint64_t workspace_bytes, void* stream) {
   if (!h_in || !h_out || !h_compressed_bytes || !d_in_scratch) return POLY_ERR_INVALID_ARG;
-  if (dt != POLY_U16 && dt != POLY_U32) return POLY_ERR_INVALID_ARG;
+  if (!dt_ok(dt)) return POLY_ERR_INVALID_ARG;
   if (n == 0) return POLY_ERR_EMPTY_INPUT;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   uint8_t* ws = reinterpret_cast<uint8_t*>(d_workspace);
@@ -1098,7 +1112,7 @@ poly_status_t poly_decompress_host(const void* h_in, uint64_t compressed_bytes, 
                                    void* d_workspace, uint64_t workspace_bytes, void* stream) {
   if (!h_in || !h_out || !h_status || !d_in_scratch || !d_out_scratch || !d_workspace)
     return POLY_ERR_INVALID_ARG;
-  if (dt != POLY_U16 && dt != POLY_U32) return POLY_ERR_INVALID_ARG;
+  if (!dt_ok(dt)) return POLY_ERR_INVALID_ARG;
   if (n == 0) return POLY_ERR_EMPTY_INPUT;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   uint8_t* ws = reinterpret_cast<uint8_t*>(d_workspace);

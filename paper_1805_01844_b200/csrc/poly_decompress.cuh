@@ -47,7 +47,7 @@ __device__ __forceinline__ uint32_t check_global_header(const DecompressArgs& a,
 
 // Validate one block header; returns POLY_ST_* bits.
 __device__ __forceinline__ uint32_t check_block(uint4 h, uint64_t nb, uint32_t width, uint32_t k) {
-  const uint64_t vmax_allowed = (width == 16) ? 0xffffull : 0xffffffffull;
+  const uint64_t vmax_allowed = (width == 32) ? 0xffffffffull : ((1ull << width) - 1);
   if (h.x == CODEC_CONSTANT) {
     uint32_t e = 0;
     if (h.z != 0 || h.w != 0) e |= POLY_ST_NWORDS;

@@ -456,10 +456,10 @@ __global__ void __launch_bounds__(PT, 1) poly_decompress_large(LargeArgs a) {
       // check_block_hdr takes a 32-bit block length: compare in 64 bits here
       if (h.x == CODEC_CONSTANT) {
         if (h.z != 0 || h.w != 0) e |= POLY_ST_NWORDS;
-        if ((uint64_t)h.y > ((sh.width == 16) ? 0xffffull : 0xffffffffull)) e |= POLY_ST_OVERFLOW;
+        if ((uint64_t)h.y > ((sh.width == 32) ? 0xffffffffull : ((1ull << sh.width) - 1))) e |= POLY_ST_OVERFLOW;
       } else if (h.x != CODEC_BASIC) {
         e |= POLY_ST_BAD_CODEC;
-      } else if (h.z == 0 || (uint64_t)h.y + h.z > ((sh.width == 16) ? 0xffffull : 0xffffffffull)) {
+      } else if (h.z == 0 || (uint64_t)h.y + h.z > ((sh.width == 32) ? 0xffffffffull : ((1ull << sh.width) - 1))) {
         e |= POLY_ST_OVERFLOW;
       } else if (W == 0 || (W - 1) * k >= nb || W * k < nb) {
         e |= POLY_ST_NWORDS;

@@ -119,6 +119,7 @@ struct PipeArgs {
   uint64_t* status;         // look-back words, one per tile
   uint32_t* ticket;
   uint32_t bulk;            // value array 16-byte aligned and tile_bytes % 16 == 0
+  uint32_t tma_shift;       // compress: array aligned, tiles not: TMA of the 16-byte aligned superset
   uint32_t debug;           // POLY_TIMING builds only (read through DBG): 1 skip compute, 2 skip look-back, ...
   uint32_t nlb;             // look-back / writer warps in use
   uint32_t server;          // 1: the last CTA is the prefix server (see prefix_server)
@@ -140,6 +141,7 @@ struct __align__(16) PipeCtl {
   uint64_t ring_end[MAXS];  // decompress: ring position after the stage's payload
   uint32_t ring_off[MAXS];  // decompress: byte offset of the stage's payload in the ring
   uint32_t err[MAXS];       // decompress: tile-level status bits
+  uint32_t shift[MAXS];     // compress: offset of the tile's first value in its stage (tma_shift)
   uint32_t done_cnt[MAXS];  // decompress: warps done with the stage
   uint32_t gnext[MAXS];     // decompress: next group (map 0) / block (map 1, G = 1) of the stage to claim
   uint64_t tfull[4], tfree[4];  // decompress maps 1, 2: staging tile filled (NCW warps) / read by its bulk store
@@ -497,6 +499,16 @@ __device__ __forceinline__ void warp_minmax(const V* s, uint32_t n, uint32_t& mn
       }
       mn = min(a0 & 0xffffu, a0 >> 16);
       mx = max(a1 & 0xffffu, a1 >> 16);
+    } else if (sizeof(V) == 1) {  // u8: four lanes of bytes per register
+      uint32_t a0 = 0xffffffffu, a1 = 0u;
+#pragma unroll 4
+      for (uint32_t i = lane; i < nq; i += 32) {
+        const uint4 t = q[i];
+        a0 = __vminu4(__vminu4(a0, __vminu4(t.x, t.y)), __vminu4(t.z, t.w));
+        a1 = __vmaxu4(__vmaxu4(a1, __vmaxu4(t.x, t.y)), __vmaxu4(t.z, t.w));
+      }
+      mn = min(min(a0 & 0xffu, (a0 >> 8) & 0xffu), min((a0 >> 16) & 0xffu, a0 >> 24));
+      mx = max(max(a1 & 0xffu, (a1 >> 8) & 0xffu), max((a1 >> 16) & 0xffu, a1 >> 24));
     } else {
 #pragma unroll 4
       for (uint32_t i = lane; i < nq; i += 32) {
@@ -517,12 +529,31 @@ __device__ __forceinline__ void warp_minmax(const V* s, uint32_t n, uint32_t& mn
 
 // Copy nbytes global -> shared by one warp (16-byte vectors when both allow).
 __device__ __forceinline__ void warp_copy(uint8_t* dst, const uint8_t* src, uint32_t nbytes, int lane) {
-  uint32_t done = 0;
-  if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
-    const uint32_t n16 = nbytes >> 4;
-    for (uint32_t i = lane; i < n16; i += 32)
-      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
-    done = n16 << 4;
+  // the widest unit both addresses share the alignment of (after a short
+  // byte head), so a tile that only starts 2-, 4- or 8-byte aligned (blocks
+  // whose byte size is not a multiple of 16) still moves in 8- or 4-byte
+  // pieces, four in flight per lane
+  const uint32_t mis = (uint32_t)((reinterpret_cast<uintptr_t>(dst) ^ reinterpret_cast<uintptr_t>(src)) & 15);
+  const uint32_t unit = (mis == 0) ? 16u : ((mis & 7) == 0) ? 8u : ((mis & 3) == 0) ? 4u : 1u;
+  uint32_t head = (uint32_t)((unit - (reinterpret_cast<uintptr_t>(src) & (unit - 1))) & (unit - 1));
+  head = min(head, nbytes);
+  if ((uint32_t)lane < head) dst[lane] = src[lane];
+  uint32_t done = head;
+  if (unit > 1) {
+    const uint32_t nu = (nbytes - head) / unit;
+    uint8_t* d = dst + head;
+    const uint8_t* s = src + head;
+    if (unit == 16) {
+#pragma unroll 4
+      for (uint32_t i = lane; i < nu; i += 32) reinterpret_cast<uint4*>(d)[i] = reinterpret_cast<const uint4*>(s)[i];
+    } else if (unit == 8) {
+#pragma unroll 4
+      for (uint32_t i = lane; i < nu; i += 32) reinterpret_cast<uint2*>(d)[i] = reinterpret_cast<const uint2*>(s)[i];
+    } else {
+#pragma unroll 4
+      for (uint32_t i = lane; i < nu; i += 32) reinterpret_cast<uint32_t*>(d)[i] = reinterpret_cast<const uint32_t*>(s)[i];
+    }
+    done = head + nu * unit;
   }
   for (uint32_t i = done + lane; i < nbytes; i += 32) dst[i] = src[i];
 }
@@ -663,19 +694,27 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       const uint64_t off = t * sh.tile_bytes;
       const uint32_t bytes = (uint32_t)min((uint64_t)sh.tile_bytes, total_bytes - off);
       const uint8_t* src = a.in + off;
-      if (a.bulk) {
+      if (a.bulk || a.tma_shift) {
+        // TMA of the 16-byte aligned range that holds the tile (blocks whose
+        // byte size is not a multiple of 16 make tiles start 2-, 4- or 8-byte
+        // aligned); the consumers start `shift` bytes into the stage.  The
+        // bytes past the last 16-byte boundary of the tile are copied by hand.
         if (lane == 0) {
-          const uint32_t b16 = bytes & ~15u;
+          const uintptr_t sa = reinterpret_cast<uintptr_t>(src), s0 = sa & ~(uintptr_t)15, e16 = (sa + bytes) & ~(uintptr_t)15;
+          const uint32_t shift = (uint32_t)(sa - s0), n16 = e16 > s0 ? (uint32_t)(e16 - s0) : 0u;
+          const uint8_t* g0 = reinterpret_cast<const uint8_t*>(s0);
           C.tkt[s] = t;
-          for (uint32_t j = b16; j < bytes; ++j) dst[j] = src[j];  // last tile only
-          mbar_arrive_tx(&C.full_in[s], b16);
-          if (b16) bulk_g2s(dst, src, b16, &C.full_in[s]);
+          C.shift[s] = shift;
+          for (uint32_t j = n16; j < shift + bytes; ++j) dst[j] = g0[j];  // the tail (the last tile, or a shifted one)
+          mbar_arrive_tx(&C.full_in[s], n16);
+          if (n16) bulk_g2s(dst, g0, n16, &C.full_in[s]);
         }
       } else {
         warp_copy(dst, src, bytes, lane);
         __syncwarp();
         if (lane == 0) {
           C.tkt[s] = t;
+          C.shift[s] = 0;
           mbar_arrive(&C.full_in[s]);
         }
       }
@@ -821,7 +860,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       }
       break;
     }
-    const V* sv = reinterpret_cast<const V*>(smem + sh.o_in + (size_t)s * sh.in_stride);
+    const V* sv = reinterpret_cast<const V*>(smem + sh.o_in + (size_t)s * sh.in_stride + C.shift[s]);
     const uint64_t b0 = t * sh.TB;
     const uint32_t nblk = (uint32_t)min((uint64_t)sh.TB, sh.n_blocks - b0);
     const uint64_t v0 = b0 * sh.Le;
@@ -1168,7 +1207,7 @@ template <typename V>
 __device__ __forceinline__ uint32_t decode_block0(const uint4 h, const uint64_t* src, uint32_t nb, uint32_t L,
                                                   uint32_t width, const BaseCache& bc, V* dst,
                                                   uint32_t jcap = 0xffffffffu, uint32_t* extra = nullptr) {
-  const uint64_t vmax = (width == 16) ? 0xffffull : 0xffffffffull;
+  const uint64_t vmax = (width == 32) ? 0xffffffffull : ((1ull << width) - 1);
   uint32_t ex0 = 0;
   if (!extra) extra = &ex0;
   *extra = 0;
@@ -1499,7 +1538,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
             bulk_wait_read<0>();
           }
         } else {
-          for (uint32_t j = lane; j < bytes; j += 32) og[j] = src[j];
+          warp_copy(og, src, bytes, lane);
         }
       }
       __syncwarp();
@@ -1578,7 +1617,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
               if (lane + 32 * i < n16) d4[32 * i] = s4[32 * i];
             for (uint32_t i = 16 * n16 + lane; i < bytes; i += 32) dst[i] = ob8[i];
           } else {
-            for (uint32_t i = lane; i < bytes; i += 32) dst[i] = ob8[i];
+            warp_copy(dst, ob8, bytes, lane);
           }
         }
         __syncwarp();

@@ -401,7 +401,7 @@ __device__ __forceinline__ uint32_t decode_any(uint64_t s, const DecConst& c, ui
 // Block-header validation (a9) without an integer divide: n_words must be
 // ceil(n_b / k), i.e. (n_words - 1) k < n_b <= n_words k.
 __device__ __forceinline__ uint32_t check_block_hdr(uint4 h, uint32_t nb, uint32_t width, uint32_t k) {
-  const uint64_t vmax_allowed = (width == 16) ? 0xffffull : 0xffffffffull;
+  const uint64_t vmax_allowed = (width == 32) ? 0xffffffffull : ((1ull << width) - 1);
   if (h.x == CODEC_CONSTANT) {
     uint32_t e = 0;
     if (h.z != 0 || h.w != 0) e |= POLY_ST_NWORDS;

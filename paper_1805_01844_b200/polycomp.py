@@ -16,6 +16,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("POLY_LIB") or os.path.join(_HERE, "libpolycomp.so")  # POLY_LIB: A/B variants
 
+POLY_U8 = 8
 POLY_U16 = 16
 POLY_U32 = 32
 
@@ -95,15 +96,17 @@ def load_library(path: str = LIB_PATH):
 
 
 def _dt(x: torch.Tensor) -> int:
+    if x.dtype == torch.uint8:
+        return POLY_U8
     if x.dtype == torch.uint16:
         return POLY_U16
     if x.dtype == torch.uint32:
         return POLY_U32
-    raise TypeError("values must be torch.uint16 or torch.uint32, got %s" % x.dtype)
+    raise TypeError("values must be torch.uint8, torch.uint16 or torch.uint32, got %s" % x.dtype)
 
 
 def _torch_dtype(dt: int) -> torch.dtype:
-    return torch.uint16 if dt == POLY_U16 else torch.uint32
+    return {POLY_U8: torch.uint8, POLY_U16: torch.uint16}.get(dt, torch.uint32)
 
 
 def _need_cuda(*ts: torch.Tensor):

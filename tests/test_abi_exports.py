@@ -55,7 +55,7 @@ def test_workspace_bytes_positive(lib):
     for n, w, L in [(1, 16, 0), (556500000, 16, 30), (1 << 28, 32, 65536), (1 << 31, 16, 4096), (1 << 20, 16, 0)]:
         assert polycomp.poly_workspace_bytes(n, w, L) >= 64
     assert polycomp.poly_workspace_bytes(0, 16, 0) == 0
-    assert polycomp.poly_workspace_bytes(10, 8, 0) == 0
+    assert polycomp.poly_workspace_bytes(10, 12, 0) == 0  # dtype 12: not a width
 
 
 def test_launches_per_call(lib):
@@ -73,7 +73,7 @@ def test_argument_errors_without_launch(lib):
     # n == 0 -> EMPTY_INPUT before anything touches CUDA
     assert lib.poly_compress(vp(16), 0, 16, 0, vp(16), 1 << 20, vp(16), vp(16), 1 << 20, None) == 2
     # bad dtype, null pointers, block_size >= 2^32
-    assert lib.poly_compress(vp(16), 10, 8, 0, vp(16), 1 << 20, vp(16), vp(16), 1 << 20, None) == 1
+    assert lib.poly_compress(vp(16), 10, 12, 0, vp(16), 1 << 20, vp(16), vp(16), 1 << 20, None) == 1
     assert lib.poly_compress(None, 10, 16, 0, vp(16), 1 << 20, vp(16), vp(16), 1 << 20, None) == 1
     assert lib.poly_compress(vp(16), 10, 16, 1 << 32, vp(16), 1 << 20, vp(16), vp(16), 1 << 20, None) == 1
     # misaligned output buffer

@@ -208,10 +208,10 @@ def test_large_blocks(oracle_lib, w, L, nblocks, tail):
 
 
 # ------------------------------------------------------------------ configs
-SMALL = {1: 1.0, 2: 1 / 100, 3: 1 / 16, 4: 1 / 128, 5: 1 / 128}  # cfg3 at 1/16: 256 blocks (large-block pipeline)
+SMALL = {1: 1.0, 2: 1 / 100, 3: 1 / 16, 4: 1 / 128, 5: 1 / 128, 6: 1 / 100}  # cfg6: cfg2 time-major  # cfg3 at 1/16: 256 blocks (large-block pipeline)
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5, 6])
 def test_config_scaled(oracle_lib, cfg):
     c = workloads.config(cfg, SMALL[cfg])
     x = workloads.generate(cfg, scale=SMALL[cfg], seed=1, device="cuda")
@@ -221,7 +221,7 @@ def test_config_scaled(oracle_lib, cfg):
     assert st == 0 and torch.equal(y, x)
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5, 6])
 def test_config_full_size(oracle_lib, cfg):
     """BASELINE.json full sizes, in the launch configuration bench.py times:
     the whole stream equals the oracle's, and decompress(compress(x)) == x."""

@@ -65,3 +65,48 @@ def test_c_oracle_corruption_status(oracle_lib):
     assert oracle_lib.decompress(s[:32] + struct.pack("<I", 9) + s[36:])[1] & oracle_lib.OST_BAD_CODEC
     assert oracle_lib.decompress(s[:-8] + struct.pack("<Q", 3 ** 40))[1] & oracle_lib.OST_RESIDUE
     assert oracle_lib.decompress(s[:36] + struct.pack("<I", 65535) + s[40:])[1] & oracle_lib.OST_OVERFLOW
+
+
+def test_u8_width_c_equals_python_and_brute_force(oracle_lib):
+    """SPEC.md:30's third width: u8 values (B <= 256, so k >= 8).  The C
+    oracle equals the Python oracle on random u8 vectors, round-trips, and its
+    size is the closed form 32 + 16 n_blocks + 8 sum ceil(n_b / k_b)."""
+    import itertools
+    import numpy as np
+    from oracle import ref
+    rng = np.random.default_rng(8)
+    for t in range(150):
+        n = int(rng.integers(1, 3000))
+        L = int(rng.choice([0, 1, 3, 8, 30, 64, 100, 1855]))
+        kind = t % 4
+        if kind == 0:
+            x = rng.integers(0, 256, n)
+        elif kind == 1:
+            x = rng.integers(100, 100 + int(rng.integers(1, 100)), n)
+        elif kind == 2:
+            x = np.full(n, int(rng.integers(0, 256)))
+        else:
+            x = np.where(rng.random(n) < 0.5, 0, 255)
+        x = x.astype(np.uint8)
+        s_c = oracle_lib.compress(x, L)
+        assert s_c == ref.compress_blocked(x.tolist(), 8, L)
+        y, st = oracle_lib.decompress(s_c)
+        assert st == 0 and np.array_equal(y, x)
+        Le = L or n
+        words = 0
+        for lo in range(0, n, Le):
+            blk = x[lo:lo + Le].astype(np.int64)
+            B = int(blk.max() - blk.min() + 1)
+            if B > 1:
+                k = 0
+                while B ** (k + 1) <= 1 << 64:
+                    k += 1
+                words += -(-blk.size // k)
+        assert len(s_c) == 32 + 16 * (-(-n // Le)) + 8 * words
+    for n in range(1, 4):   # brute force over tiny u8 vectors
+        for v in itertools.product([0, 1, 2, 127, 255], repeat=n):
+            x = np.array(v, dtype=np.uint8)
+            for L in range(0, n + 2):
+                s = oracle_lib.compress(x, L)
+                assert s == ref.compress_blocked(list(v), 8, L)
+                assert np.array_equal(oracle_lib.decompress(s)[0], x)

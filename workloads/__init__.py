@@ -17,6 +17,10 @@ Recipes:
         probability 1e-4, L = 1,024.
   cfg5  2^31 u16, L = 4,096; block i mod 3: 0 -> Poisson(20),
         1 -> round(N(1000, 30^2)), 2 -> uniform integers [0, 15].
+  cfg6  cfg2's values in the paper's time-major matrix layout M_{i,j}
+        (PAPER.md:457-460, "M_{i,j} corresponds to the i-th time"): per
+        event a [30 time samples][1855 pixels] matrix, row-major, one block
+        per time row (L = 1855) -- SURVEY.md Sec. 8(f) row 4.
 `scale` < 1 shrinks the number of events / blocks / values while keeping the
 distribution, the block length and the layout (used by the CPU-sized tests).
 """
@@ -63,7 +67,11 @@ def config(cfg: int, scale: float = 1.0) -> Config:
         n = max(4096 * 3, int((1 << 31) * scale))
         return Config("cfg5_mixed_blocks_u16", torch.uint16, n, 4096,
                       "u16 L=4096 cycling Poisson(20) / N(1000,30^2) / U[0,15]")
-    raise ValueError("cfg must be 1..5")
+    if cfg == 6:
+        ev = max(1, int(CTA_EVENTS * scale))
+        return Config("cfg6_cta_time_major", torch.uint16, ev * CTA_PIXELS * CTA_SAMPLES, CTA_PIXELS,
+                      "%d events x 30 samples x 1855 pixels u16 (time-major M_ij), L=1855" % ev)
+    raise ValueError("cfg must be 1..6")
 
 
 def _gen(device, seed):
@@ -139,5 +147,16 @@ def generate(cfg: int, scale: float = 1.0, seed: int = 0, device="cpu") -> torch
             lo = b0 * L
             hi = min(c.n, b1 * L)
             out[lo:hi] = flat[: hi - lo]
+        return out
+    if cfg == 6:  # cfg2's values, each event's [pixel][time] matrix transposed to [time][pixel]
+        x = generate(2, scale=scale, seed=seed, device=device)
+        ev = c.n // (CTA_PIXELS * CTA_SAMPLES)
+        out = torch.empty_like(x)
+        per = max(1, CHUNK // (CTA_PIXELS * CTA_SAMPLES))
+        for e0 in range(0, ev, per):
+            e1 = min(ev, e0 + per)
+            blk = x[e0 * CTA_PIXELS * CTA_SAMPLES: e1 * CTA_PIXELS * CTA_SAMPLES].view(torch.int16)
+            blk = blk.view(e1 - e0, CTA_PIXELS, CTA_SAMPLES).transpose(1, 2).contiguous().view(-1)
+            out.view(torch.int16)[e0 * CTA_PIXELS * CTA_SAMPLES: e1 * CTA_PIXELS * CTA_SAMPLES] = blk
         return out
     raise ValueError(cfg)
