@@ -12,6 +12,7 @@
 #include "poly_pipe.cuh"
 #include "poly_large.cuh"
 #include "poly_adv.cuh"
+#include "poly_dec3.cuh"
 
 #include <vector>
 
@@ -306,6 +307,7 @@ void set_attrs(int pmax) {
   set_smem_attr(poly_decompress_unpack<V>, large_smem_unpack<V>());
   set_smem_attr(poly_decompress_large1<V>, large_smem_unpack<V>());
   set_smem_attr(poly_compress_large1<V>, large_smem_pack<V>());
+  set_smem_attr(d3::dec3_main<V>, 227 * 1024);
 }
 
 poly_status_t ensure_init(int dev) {
@@ -508,6 +510,59 @@ bool plan(uint64_t n, uint32_t w, uint64_t block_size, Shape& sh, Regime& rg) {
     sh.n_stiles = (sh.n_blocks + SCAN_T - 1) / SCAN_T;
   }
   return true;
+}
+
+// ---------------------------------------------------------------- dec3
+// Two-pass decompress of the map-1 regime (128 B < block <= 32 KiB,
+// poly_dec3.cuh): shapes, shared memory, workspace.
+struct Dec3Plan {
+  d3::Args a;
+  uint32_t smem;
+  uint64_t ws_bytes, o_cw, o_cu, o_T;
+};
+uint64_t dec3_units_max(uint64_t blen, uint32_t ut, uint32_t kmin) {
+  uint64_t m = 1;
+  for (uint32_t k = kmin; k <= 64; ++k) {
+    uint32_t w = (ut / k) & ~7u;
+    if (w < 8) w = 8;
+    const uint64_t nw = (blen + k - 1) / k;
+    m = std::max<uint64_t>(m, (nw + w - 1) / w);
+  }
+  return m;
+}
+bool plan_dec3(const Shape& sh, Dec3Plan& P) {
+  memset(&P, 0, sizeof P);
+  d3::Args& a = P.a;
+  a.n = sh.n;
+  a.Le = sh.Le;
+  a.n_blocks = sh.n_blocks;
+  a.last_len = sh.n - (sh.n_blocks - 1) * sh.Le;
+  a.block_len = sh.block_len;
+  a.width = sh.width;
+  a.vb = sh.width / 8;
+  a.kmin_log2 = sh.width == 8 ? 3u : (sh.width == 16 ? 2u : 1u);
+  a.ut = 4096 / a.vb;
+  a.n_chunks = (sh.n_blocks + d3::CE - 1) / d3::CE;
+  const uint32_t kmin = 1u << a.kmin_log2;
+  a.max_units = (sh.n_blocks - 1) * dec3_units_max(sh.Le, a.ut, kmin) + dec3_units_max(a.last_len, a.ut, kmin);
+  a.cap = (uint32_t)((a.ut * a.vb + 32 + 15) / 16 * 16);
+  a.o_warp = (uint32_t)((sizeof(d3::Ctl) + 127) / 128 * 128);
+  a.o_ring = (a.o_warp + d3::NW * a.cap + 127) / 128 * 128;
+  const uint32_t smax = 227 * 1024;
+  a.ring_bytes = (smax - a.o_ring) / 16 * 16;
+  // worst tile: TU units of <= ut / k_min + 8 words, their headers, the table entries
+  const uint64_t worst = 16ull * d3::TU + 16ull * (d3::TU + 1) + 8ull * d3::TU * (a.ut / kmin + 8) + 64;
+  if (worst > a.ring_bytes / 2) return false;
+  P.smem = smax;
+  P.o_cw = 64;
+  P.o_cu = 64 + 8 * a.n_chunks;
+  P.o_T = (P.o_cu + 8 * a.n_chunks + 15) / 16 * 16;
+  P.ws_bytes = P.o_T + 16 * (a.max_units + 1);
+  return true;
+}
+bool use_dec3(const Shape& sh) {
+  const uint64_t bb = sh.Le * (sh.width / 8);
+  return bb > MAP0_MAX_BLOCK && bb <= PIPE_MAX_BLOCK;
 }
 
 struct WsLayout {
@@ -737,7 +792,10 @@ uint64_t poly_workspace_bytes(uint64_t n, poly_dtype_t dt, uint64_t block_size) 
   Shape sh;
   Regime rg;
   if (!plan(n, (uint32_t)dt, block_size, sh, rg)) return 0;
-  return ws_layout(sh, rg).total;
+  uint64_t t = ws_layout(sh, rg).total;
+  Dec3Plan dp;
+  if (rg == PIPE && use_dec3(sh) && plan_dec3(sh, dp)) t = std::max<uint64_t>(t, dp.ws_bytes);
+  return t;
 }
 
 #ifdef POLY_TRACE
@@ -758,6 +816,7 @@ int poly_launches_per_call(uint64_t n, poly_dtype_t dt, uint64_t block_size, int
   Shape sh;
   Regime rg;
   if (!plan(n, (uint32_t)dt, block_size, sh, rg)) return 0;
+  if (decompress && rg == PIPE && use_dec3(sh)) return 2;  // unit table + decode (poly_dec3.cuh)
   if (rg == PIPE || rg == LARGE2) return 1;
   if (decompress) return large1_decompress(sh) ? 1 : 2;
   return large1_compress(sh) ? 1 : 3;
@@ -892,6 +951,29 @@ poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_
   a.status = reinterpret_cast<uint64_t*>(ws + W.status_off);
   a.sh = sh;
   cudaMemsetAsync(d_status, 0, 4, s);
+  Dec3Plan dp;
+  if (rg == PIPE && use_dec3(sh) && plan_dec3(sh, dp)) {
+    if (workspace_bytes < dp.ws_bytes) return POLY_ERR_WORKSPACE;
+    d3::Args d = dp.a;
+    d.in = a.in;
+    d.in_bytes = compressed_bytes;
+    d.out = reinterpret_cast<uint8_t*>(d_out);
+    d.status_out = d_status;
+    d.ticket = reinterpret_cast<uint32_t*>(ws);
+    d.abort_flag = reinterpret_cast<uint32_t*>(ws + 4);
+    d.n_units = reinterpret_cast<uint64_t*>(ws + 8);
+    d.cst_w = reinterpret_cast<uint64_t*>(ws + dp.o_cw);
+    d.cst_u = reinterpret_cast<uint64_t*>(ws + dp.o_cu);
+    d.T = reinterpret_cast<uint4*>(ws + dp.o_T);
+    d.kw_ok = (dt == POLY_U16 && (reinterpret_cast<uintptr_t>(d_out) & 15) == 0 && (sh.Le * 2) % 16 == 0) ? 1u : 0u;
+    cudaMemsetAsync(ws, 0, dp.o_T, s);
+    const uint64_t sms = (uint64_t)(g_sms[dev] > 0 ? g_sms[dev] : 148);
+    const unsigned g1 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(d.n_chunks, 4 * sms));
+    d3::dec3_offsets<<<g1, d3::K1T, 0, s>>>(d);
+    POLY_DISPATCH(dt, { d3::dec3_main<V><<<(unsigned)sms, d3::NTHR, dp.smem, s>>>(d); });
+    if (cudaGetLastError() != cudaSuccess) return POLY_ERR_CUDA;
+    return POLY_OK;
+  }
   if (rg == LARGE2) {
     cudaMemsetAsync(ws, 0, W.total, s);
     LargeArgs la;
