@@ -278,6 +278,38 @@ __device__ __forceinline__ uint32_t dec_word(uint64_t s, const Blk& c, uint32_t 
 // are computed but not stored.
 
 
+// A word of capacity k from the table constants alone (no premultiplier):
+// its m <= k digits are the last m of k steps; the first k - m (above the
+// word's top digit) must be 0, else POLY_ST_RESIDUE (s >= B^m).  first[0..m)
+// receives v_min + digits, lowest power first.
+template <typename V>
+__device__ __forceinline__ uint32_t dec_word_dc(uint64_t s, const DecConst& dc, uint32_t B, uint32_t vmin, uint32_t k,
+                                                uint32_t m, V* first) {
+  const uint32_t add = ((dc.meta >> 8) & 0xffu) ? 0u : 1u, t32 = (dc.meta >> 16) & 0xffu;
+  uint32_t err = 0;
+  const uint64_t hi1 = __umul64hi(s, dc.Rl), lo2 = s * dc.Rh, hi2 = __umul64hi(s, dc.Rh);
+  const uint64_t mid = lo2 + hi1, t = hi2 + (mid < lo2 ? 1ull : 0ull);
+  if (t >> 32) err = POLY_ST_RESIDUE;
+  const uint64_t f = (t << 32) + (mid >> 32) + add;
+  uint32_t f0 = (uint32_t)f, f1 = (uint32_t)(f >> 32), zero = 0;
+  const uint32_t n64 = k - t32;  // steps before the 32-bit phase
+  uint32_t i = 0;
+#pragma unroll 1
+  for (; i < n64; ++i) {
+    const uint32_t d = fstep64(f0, f1, B, 0u);
+    if (i < k - m) zero |= d;
+    else first[k - 1 - i] = (V)(vmin + d);
+  }
+  uint32_t g = f1 + add;
+#pragma unroll 1
+  for (; i < k; ++i) {
+    const uint32_t d = fstep32(g, B, 0u);
+    if (i < k - m) zero |= d;
+    else first[k - 1 - i] = (V)(vmin + d);
+  }
+  return (err | (zero ? POLY_ST_RESIDUE : 0u));
+}
+
 // ------------------------------------------------------------------ output
 // Copy the global byte range [c_lo, c_hi) from the staging buffer, whose byte
 // x holds global byte G0 + x (G0 16-byte aligned): 16-byte stores inside,
@@ -629,44 +661,67 @@ __global__ void __launch_bounds__(NTHR, 1) dec3_main(Args a) {
       const uint64_t* PAY = reinterpret_cast<const uint64_t*>(ring + S.off_p) + (wst - S.ws);
       const uint4 h = reinterpret_cast<const uint4*>(ring + S.off_h)[b - S.hb0];
       const uint32_t blen = block_len_of(a, b);
-      uint32_t e1 = 0;
-      nw_clamp(a, h.w, blen, e1);
-      const Blk c = block_consts(a, h, blen, e1);
-      if (j0 == 0) err |= e1;  // reported once per block
       const uint64_t gblk = reinterpret_cast<uint64_t>(a.out) + b * a.Le * sizeof(V);
-      if (c.kind == 1) {
-        fill_out<V>(gblk, gblk + (uint64_t)blen * sizeof(V), c.vmin, lane);
-      } else if (c.kind == 2) {
-        const uint32_t k = c.k, j1 = j0 + nwu;
-        const uint64_t gbase = gblk + (uint64_t)j0 * k * sizeof(V);
-        const uint64_t G0 = gbase & ~15ull;
-        V* stgv = reinterpret_cast<V*>(stg + (gbase - G0));  // staging value t <-> block value j0 k + t
-        const uint32_t nfull = c.mtop < k ? c.nw - 1 : c.nw;  // words with all k digits
-        uint32_t jdone = j0;  // words [j0, jdone) decoded by the group codec
-        if (sizeof(V) == 2 && a.kw_ok && !c.b32) {
-          uint8_t* blk = reinterpret_cast<uint8_t*>(stgv) - 2ull * j0 * k;  // block value 0 (never dereferenced below j0 k)
-          const DecConst dc = g_dtab[c.bm1 + 1];
-          const uint32_t B = c.bm1 + 1, jf = min(j1, nfull);
+      const uint32_t B = h.z + 1;
+      // fast path: a valid u16 BASIC block that starts 16-byte aligned, a
+      // capacity with a k-specialised group codec; the header checks of
+      // block_consts, in its order, without the premultiplier
+      bool fast = false;
+      if (sizeof(V) == 2 && a.kw_ok && h.x == CODEC_BASIC && h.z != 0 && h.y + h.z <= 0xffffu) {
+        const DecConst dc = g_dtab[B];
+        const uint32_t k = dc.meta & 0xffu, nw = h.w;
+        const bool nw_ok = nw != 0 && (nw - 1) * k < blen && nw * k >= blen;
+        if (nw_ok && k >= 4 && k <= 27 && k != 23 && k != 25 && k != 26) {
+          fast = true;
+          const uint32_t j1 = j0 + nwu, mtop = blen - (nw - 1) * k;
+          const uint32_t nfull = mtop < k ? nw - 1 : nw, jf = min(j1, nfull);
+          const uint64_t gbase = gblk + (uint64_t)j0 * k * 2;  // 16-byte aligned (kw_ok, j0 % 8 == 0)
+          uint8_t* blk = stg - 2ull * j0 * k;                 // block value 0 in staging coordinates
+          const bool p2 = dc_log2b(dc) != 0;
+          uint32_t jdone = j0;
           switch (k) {
-#define POLY_D3K(KK)                                                                          \
-  case KK: {                                                                                  \
-    const uint32_t gb = j0 / kq<KK>(), ge = jf / kq<KK>();                                    \
-    if (ge > gb) err |= unpack_groups_k<KK>(PAY - j0, gb, ge, dc, B, c.vmin, blk);            \
-    jdone = max(j0, ge * kq<KK>());                                                           \
+#define POLY_D3K(KK)                                                                             \
+  case KK: {                                                                                     \
+    const uint32_t gb = j0 / kq<KK>(), ge = jf / kq<KK>();                                       \
+    if (ge > gb)                                                                                 \
+      err |= p2 ? unpack_groups_kp<KK, true>(PAY - j0, gb, ge, dc, B, h.y, blk)                  \
+                : unpack_groups_kp<KK, false>(PAY - j0, gb, ge, dc, B, h.y, blk);                \
+    jdone = max(j0, ge * kq<KK>());                                                              \
   } break;
             POLY_FOR_EACH_K16(POLY_D3K)
 #undef POLY_D3K
             default:
               break;
           }
+          for (uint32_t j = jdone + lane; j < j1; j += 32) {  // the odd word of a pair and / or the block's last word
+            const uint32_t m = (j + 1 == nw) ? mtop : k;
+            err |= dec_word_dc<V>(PAY[j - j0], dc, B, h.y, k, m, reinterpret_cast<V*>(stg) + (j - j0) * k);
+          }
+          __syncwarp();
+          const uint32_t nv = min(blen, j1 * k) - j0 * k;
+          copy_out<V>(stg, gbase, gbase, gbase + (uint64_t)nv * 2, lane);
         }
-        for (uint32_t j = jdone + lane; j < j1; j += 32) {  // the rest: one word per lane
-          const uint32_t m = (j + 1 == c.nw) ? c.mtop : k;
-          err |= dec_word<V>(PAY[j - j0], c, m, stgv + (j - j0) * k + (m - 1));
+      }
+      if (!fast) {
+        uint32_t e1 = 0;
+        nw_clamp(a, h.w, blen, e1);
+        const Blk c = block_consts(a, h, blen, e1);
+        if (j0 == 0) err |= e1;  // reported once per block
+        if (c.kind == 1) {
+          fill_out<V>(gblk, gblk + (uint64_t)blen * sizeof(V), c.vmin, lane);
+        } else if (c.kind == 2) {
+          const uint32_t k = c.k, j1 = j0 + nwu;
+          const uint64_t gbase = gblk + (uint64_t)j0 * k * sizeof(V);
+          const uint64_t G0 = gbase & ~15ull;
+          V* stgv = reinterpret_cast<V*>(stg + (gbase - G0));  // staging value t <-> block value j0 k + t
+          for (uint32_t j = j0 + lane; j < j1; j += 32) {
+            const uint32_t m = (j + 1 == c.nw) ? c.mtop : k;
+            err |= dec_word<V>(PAY[j - j0], c, m, stgv + (j - j0) * k + (m - 1));
+          }
+          __syncwarp();
+          const uint32_t nv = (uint32_t)min((uint64_t)blen, (uint64_t)j1 * k) - j0 * k;
+          copy_out<V>(stg, G0, gbase, gbase + (uint64_t)nv * sizeof(V), lane);
         }
-        __syncwarp();
-        const uint32_t nv = (uint32_t)min((uint64_t)blen, (uint64_t)j1 * k) - j0 * k;
-        copy_out<V>(stg, G0, gbase, gbase + (uint64_t)nv * sizeof(V), lane);
       }
     }
     __syncwarp();

@@ -247,4 +247,68 @@ __device__ __forceinline__ uint32_t unpack_block_k(const uint64_t* src, uint32_t
   return err;
 }
 
+// Unpack group g with the base class fixed at compile time (POW2: B = 2^j,
+// digits are bit fields; else binary-fraction steps), so neither path is
+// if-converted into the other (poly_dec3.cuh).
+template <int K, bool POW2>
+__device__ __forceinline__ uint32_t unpack_group_p(const uint64_t* src, uint32_t g, const DecConst& dc, uint32_t B,
+                                                   uint32_t vmin, uint8_t* blk) {
+  using C = KCls<K>;
+  constexpr int T = t32min_u16(K);
+  uint32_t r[C::NR];
+  uint32_t err = 0;
+#pragma unroll
+  for (int q = 0; q < C::Q; ++q) {
+    const uint64_t s = src[g * C::Q + q];
+    const int o = q * K;
+    uint32_t d[K];
+    if (POW2) {
+      const uint32_t j = dc_log2b(dc);
+#pragma unroll
+      for (int i = 0; i < K; ++i) d[i] = ((uint32_t)(s >> (i * j)) & (B - 1)) + vmin;
+      if (K * j < 64 && (s >> (K * j)) != 0) err = POLY_ST_RESIDUE;
+    } else {
+      if (s > dc.Wmax) err = POLY_ST_RESIDUE;
+      const uint64_t hi1 = __umul64hi(s, dc.Rl);
+      const uint64_t lo2 = s * dc.Rh;
+      const uint64_t hi2 = __umul64hi(s, dc.Rh);
+      const uint64_t mid = lo2 + hi1;
+      const uint64_t f = ((hi2 + (mid < lo2 ? 1ull : 0ull)) << 32) + (mid >> 32) + 1;
+      uint32_t f0 = (uint32_t)f, f1 = (uint32_t)(f >> 32);
+#pragma unroll
+      for (int i = K - 1; i >= T; --i) {
+        const uint64_t t0 = (uint64_t)f0 * B;
+        const uint64_t t1 = (uint64_t)f1 * B + (uint32_t)(t0 >> 32);
+        d[i] = (uint32_t)(t1 >> 32) + vmin;
+        f1 = (uint32_t)t1;
+        f0 = (uint32_t)t0;
+      }
+      uint32_t gg = f1 + 1;
+#pragma unroll
+      for (int i = T - 1; i >= 0; --i) {
+        const uint64_t p = (uint64_t)gg * B;
+        d[i] = (uint32_t)(p >> 32) + vmin;
+        gg = (uint32_t)p;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const int idx = o + i;
+      if (idx & 1)
+        r[idx >> 1] = __byte_perm(r[idx >> 1], d[i], 0x5410);
+      else
+        r[idx >> 1] = d[i];
+    }
+  }
+  store_group<K>(blk + (size_t)g * C::BYTES, r);
+  return err;
+}
+template <int K, bool POW2>
+__device__ __forceinline__ uint32_t unpack_groups_kp(const uint64_t* src, uint32_t gb, uint32_t ge, const DecConst& dc,
+                                                     uint32_t B, uint32_t vmin, uint8_t* blk) {
+  uint32_t err = 0;
+  for (uint32_t g = gb + (threadIdx.x & 31); g < ge; g += 32) err |= unpack_group_p<K, POW2>(src, g, dc, B, vmin, blk);
+  return err;
+}
+
 }  // namespace polyk
