@@ -970,9 +970,9 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
         }
       }
     } else {
-      const uint32_t G = sh.G, nseg = nblk * G;
+      const uint32_t lg = __ffs(sh.G) - 1, G = sh.G, nseg = nblk << lg;  // G: a power of two
       for (uint32_t seg = warp; seg < nseg; seg += NCW) {
-        const uint32_t b = seg / G, part = seg % G;
+        const uint32_t b = seg >> lg, part = seg & (G - 1);
         const uint32_t nb = min(L, nv - b * L);
         const uint32_t lo = min(nb, part * sh.Lp), hi = min(nb, lo + sh.Lp);
         uint32_t mn, mx;
@@ -983,22 +983,28 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
         }
       }
       cons_bar<NW>();
-      uint32_t nwb = 0;
-      if (ctid < (int)nblk) {
-        uint32_t mn = 0xffffffffu, mx = 0u;
-        for (uint32_t p = 0; p < G; ++p) {
-          mn = min(mn, C.smin[ctid * G + p]);
-          mx = max(mx, C.smax[ctid * G + p]);
+      // per-block reduction of the segments and the in-tile word offsets: by
+      // warp 0 alone when the tile has at most 32 blocks (no CTA scan, the
+      // other warps go straight to the barrier before the pack)
+      const bool w0 = nblk <= 32;
+      if (!w0 || warp == 0) {
+        uint32_t nwb = 0;
+        if (ctid < (int)nblk) {
+          uint32_t mn = 0xffffffffu, mx = 0u;
+          for (uint32_t p = 0; p < G; ++p) {
+            mn = min(mn, C.smin[(ctid << lg) + p]);
+            mx = max(mx, C.smax[(ctid << lg) + p]);
+          }
+          const uint32_t nb = min(L, nv - ctid * L);
+          if (mx != mn) nwb = ceil_div_small(nb, k_of(bc, (uint64_t)(mx - mn) + 1));
+          C.bvmin[ctid] = mn;
+          C.bbm1[ctid] = mx - mn;
+          C.bnw[ctid] = nwb;
+          hdr_g[b0 + ctid] = make_uint4(mx == mn ? CODEC_CONSTANT : CODEC_BASIC, mn, mx - mn, nwb);
         }
-        const uint32_t nb = min(L, nv - ctid * L);
-        if (mx != mn) nwb = ceil_div_small(nb, k_of(bc, (uint64_t)(mx - mn) + 1));
-        C.bvmin[ctid] = mn;
-        C.bbm1[ctid] = mx - mn;
-        C.bnw[ctid] = nwb;
-        hdr_g[b0 + ctid] = make_uint4(mx == mn ? CODEC_CONSTANT : CODEC_BASIC, mn, mx - mn, nwb);
+        const uint32_t ex = w0 ? warp_excl_scan(nwb, &W) : cons_scan<NW>(nwb, &W, C.scan[0]);
+        if (ctid < (int)nblk) C.boff[ctid] = ex;
       }
-      const uint32_t ex = cons_scan<NW>(nwb, &W, C.scan[0]);
-      if (ctid < (int)nblk) C.boff[ctid] = ex;
     }
     // ---- a4: publish the tile aggregate, then take ring space for its words
     if (ctid == 0) {
@@ -1047,9 +1053,9 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
         }
       }
     } else {
-      const uint32_t G = sh.G, nseg = nblk * G;
+      const uint32_t lg = __ffs(sh.G) - 1, G = sh.G, nseg = nblk << lg;
       for (uint32_t seg = warp; seg < nseg; seg += NCW) {
-        const uint32_t b = seg / G, part = seg % G;
+        const uint32_t b = seg >> lg, part = seg & (G - 1);
         const uint32_t bm1b = C.bbm1[b];
         if (bm1b == 0) continue;
         const uint32_t nb = min(L, nv - b * L), nwk = C.bnw[b], vm = C.bvmin[b];
