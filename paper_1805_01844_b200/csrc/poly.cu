@@ -46,6 +46,9 @@ namespace {
 #ifndef POLY_NCW_C
 #define POLY_NCW_C 24
 #endif
+#ifndef POLY_NCW_C2
+#define POLY_NCW_C2 12
+#endif
 #ifndef POLY_NCW_D0
 #define POLY_NCW_D0 26
 #endif
@@ -55,7 +58,7 @@ namespace {
 #ifndef POLY_NCW_D1B
 #define POLY_NCW_D1B 12
 #endif
-constexpr int NCW_C = POLY_NCW_C, NCW_D0 = POLY_NCW_D0, NCW_D1 = POLY_NCW_D1, NCW_D1B = POLY_NCW_D1B;
+constexpr int NCW_C = POLY_NCW_C, NCW_C2 = POLY_NCW_C2, NCW_D0 = POLY_NCW_D0, NCW_D1 = POLY_NCW_D1, NCW_D1B = POLY_NCW_D1B;
 // Compress: worst-case tiles the word ring is guaranteed to hold (the input
 // stages get the rest first).  At least 2: a tile's words stay contiguous, so
 // an allocation that wraps skips the ring's tail end (1 tile can deadlock).
@@ -298,6 +301,7 @@ template <typename V>
 void set_attrs(int pmax) {
   set_smem_attr(poly_compress_pipe<V, 0, NCW_C>, pmax);
   set_smem_attr(poly_compress_pipe<V, 1, NCW_C>, pmax);
+  set_smem_attr(poly_compress_pipe<V, 1, NCW_C2>, pmax);
   set_smem_attr(poly_decompress_pipe<V, 0, NCW_D0>, pmax);
   set_smem_attr(poly_decompress_pipe<V, 1, NCW_D1>, pmax);
   set_smem_attr(poly_decompress_pipe<V, 1, NCW_D1B>, pmax);
@@ -436,7 +440,17 @@ bool plan_pipe_n(const Shape& sh, PipeShape& ps, bool decomp, uint32_t ncw) {
 // parts 1751 GB/s vs 16 / 2 KiB 1439; cfg4 16 warps).
 bool plan_pipe(const Shape& sh, PipeShape& ps, bool decomp) {
   const bool map0 = (uint64_t)sh.Le * (sh.width / 8) <= MAP0_MAX_BLOCK;
-  if (!decomp) return plan_pipe_n(sh, ps, false, NCW_C);
+  if (!decomp) {
+    // map 1: NCW_C2 warps when NCW_C would split each block over 4 or more
+    // warps and the smaller count keeps the tile (measured, cfg5: 24 warps /
+    // 1024-value parts 2725 GB/s, 12 / 2048 2980; cfg6, G 2 -> 1, and cfg4,
+    // G = 1 either way, keep NCW_C)
+    if (!plan_pipe_n(sh, ps, false, NCW_C)) return false;
+    PipeShape b;
+    if (ps.map == 1 && ps.G >= 4 && plan_pipe_n(sh, b, false, NCW_C2) && b.G < ps.G && b.tile_bytes == ps.tile_bytes)
+      ps = b;
+    return true;
+  }
   if (map0) return plan_pipe_n(sh, ps, true, NCW_D0);
   PipeShape a, b;
   const bool oa = plan_pipe_n(sh, a, true, NCW_D1), ob = plan_pipe_n(sh, b, true, NCW_D1B);
@@ -686,9 +700,12 @@ void launch_compress_pipe(const Shape& sh, poly_dtype_t dt, const void* d_in, ui
   const bool wr = pa.sh.wrings != 0;
   pa.nlb = lb_warps(wr ? 4 : 2, NLB_MAX + 1);
   POLY_DISPATCH(dt, {
-    auto k = pa.sh.map == 0 ? poly_compress_pipe<V, 0, NCW_C> : poly_compress_pipe<V, 1, NCW_C>;
-    const int grid = pipe_grid_server(k, pipe_threads(NCW_C), pa.sh.smem, pa.t_end - pa.t_begin, dev, pa.server);
-    launch_k(k, grid, pipe_threads(NCW_C), pa.sh.smem, s, pa.server != 0, pa);
+    auto k = pa.sh.map == 0         ? poly_compress_pipe<V, 0, NCW_C>
+             : pa.sh.ncw == NCW_C ? poly_compress_pipe<V, 1, NCW_C>
+                                  : poly_compress_pipe<V, 1, NCW_C2>;
+    const int nt = pipe_threads((int)pa.sh.ncw);
+    const int grid = pipe_grid_server(k, nt, pa.sh.smem, pa.t_end - pa.t_begin, dev, pa.server);
+    launch_k(k, grid, nt, pa.sh.smem, s, pa.server != 0, pa);
   });
 }
 
