@@ -677,12 +677,17 @@ __global__ void __launch_bounds__(NTHR, 1) dec3_main(Args a) {
           const uint32_t nfull = mtop < k ? nw - 1 : nw, jf = min(j1, nfull);
           const uint64_t gbase = gblk + (uint64_t)j0 * k * 2;  // 16-byte aligned (kw_ok, j0 % 8 == 0)
           uint8_t* blk = stg - 2ull * j0 * k;                 // block value 0 in staging coordinates
-          const bool p2 = dc_log2b(dc) != 0;
+          const uint32_t lj = dc_log2b(dc);
+          const bool p2 = lj != 0;
           uint32_t jdone = j0;
           switch (k) {
 #define POLY_D3K(KK)                                                                             \
   case KK: {                                                                                     \
-    const uint32_t gb = j0 / kq<KK>(), ge = jf / kq<KK>();                                       \
+    /* the group codec's power-of-two path is for B = 2^(64 / KK); the other \
+       power-of-two bases of capacity KK (2^11 for 5, 2^13..2^15 for 4) go  \
+       word by word below */                                                \
+    const uint32_t gb = j0 / kq<KK>();                                                           \
+    const uint32_t ge = (!p2 || lj == 64 / KK) ? jf / kq<KK>() : gb;                             \
     if (ge > gb)                                                                                 \
       err |= p2 ? unpack_groups_kp<KK, true>(PAY - j0, gb, ge, dc, B, h.y, blk)                  \
                 : unpack_groups_kp<KK, false>(PAY - j0, gb, ge, dc, B, h.y, blk);                \

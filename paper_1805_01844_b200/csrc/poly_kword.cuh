@@ -257,17 +257,38 @@ __device__ __forceinline__ uint32_t unpack_group_p(const uint64_t* src, uint32_t
   constexpr int T = t32min_u16(K);
   uint32_t r[C::NR];
   uint32_t err = 0;
+  if (POW2) {
+    // B = 2^J with J = 64 / K (the one power-of-two base of capacity K, when
+    // there is one): two J-bit fields per 32-bit register by constant shifts,
+    // vmin added to both halves at once (digit + vmin <= 65535: no carry)
+    constexpr int J = 64 / K;
+    constexpr uint32_t M = (1u << J) - 1u;
+    const uint32_t vmin2 = vmin * 0x10001u;
+    uint64_t w[C::Q];
 #pragma unroll
-  for (int q = 0; q < C::Q; ++q) {
-    const uint64_t s = src[g * C::Q + q];
-    const int o = q * K;
-    uint32_t d[K];
-    if (POW2) {
-      const uint32_t j = dc_log2b(dc);
+    for (int q = 0; q < C::Q; ++q) {
+      w[q] = src[g * C::Q + q];
+      if (K * J < 64 && (w[q] >> (K * J)) != 0) err = POLY_ST_RESIDUE;
+    }
 #pragma unroll
-      for (int i = 0; i < K; ++i) d[i] = ((uint32_t)(s >> (i * j)) & (B - 1)) + vmin;
-      if (K * j < 64 && (s >> (K * j)) != 0) err = POLY_ST_RESIDUE;
-    } else {
+    for (int p = 0; p < C::NR; ++p) {
+      const int q0 = (2 * p) / K, e0 = (2 * p) % K, q1 = (2 * p + 1) / K, e1 = (2 * p + 1) % K;
+      if (q0 == q1) {
+        const uint32_t x = (uint32_t)(w[q0] >> (e0 * J));
+        r[p] = ((x & M) | ((x << (16 - J)) & (M << 16))) + vmin2;
+      } else {  // the pair straddles the group's two words (odd K)
+        const uint32_t d0 = (uint32_t)(w[q0] >> (e0 * J)) & M, d1 = (uint32_t)(w[q1] >> (e1 * J)) & M;
+        r[p] = (d0 | (d1 << 16)) + vmin2;
+      }
+    }
+    (void)B;
+    (void)dc;
+  } else {
+#pragma unroll
+    for (int q = 0; q < C::Q; ++q) {
+      const uint64_t s = src[g * C::Q + q];
+      const int o = q * K;
+      uint32_t d[K];
       if (s > dc.Wmax) err = POLY_ST_RESIDUE;
       const uint64_t hi1 = __umul64hi(s, dc.Rl);
       const uint64_t lo2 = s * dc.Rh;
@@ -290,14 +311,14 @@ __device__ __forceinline__ uint32_t unpack_group_p(const uint64_t* src, uint32_t
         d[i] = (uint32_t)(p >> 32) + vmin;
         gg = (uint32_t)p;
       }
-    }
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
-      const int idx = o + i;
-      if (idx & 1)
-        r[idx >> 1] = __byte_perm(r[idx >> 1], d[i], 0x5410);
-      else
-        r[idx >> 1] = d[i];
+      for (int i = 0; i < K; ++i) {
+        const int idx = o + i;
+        if (idx & 1)
+          r[idx >> 1] = __byte_perm(r[idx >> 1], d[i], 0x5410);
+        else
+          r[idx >> 1] = d[i];
+      }
     }
   }
   store_group<K>(blk + (size_t)g * C::BYTES, r);
