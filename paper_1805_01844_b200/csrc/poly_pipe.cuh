@@ -156,6 +156,7 @@ struct __align__(16) PipeCtl {
   volatile uint64_t ring_tail;  // decompress: ring bytes released by the consumers
   volatile uint32_t lb_seq;     // decompress: next stage to take ring space
   uint64_t ring_head;           // decompress: ring bytes handed out
+  uint32_t ring_hpos, pad2;     // decompress: ring_head modulo the ring size
   uint32_t hdr_err, pad;
   uint32_t nwL[68];             // compress map 0: ceil(L / k) for k = 1..64
   // compress map 0 with one block per consumer thread (bpt = 1): per-warp word
@@ -842,6 +843,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
   uint4* hdr_g = reinterpret_cast<uint4*>(a.out + 32);
   uint64_t head = 0;  // ring bytes handed out (thread 0's copy is authoritative)
   uint64_t whead = 0;  // WARP_RINGS: this warp's ring bytes handed out (lane 0)
+  uint32_t hpos = 0;   // head (or whead) modulo the ring size, kept incrementally
   for (uint32_t s = 0, ph = 0, r = 0, rph = 0, it = 0;;
        s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0), r = (r + 1) % MAXR, rph ^= (r == 0), ++it) {
     mbar_wait_cmp<POLY_CMP_PARK_IN>(&C.full_in[s], ph);
@@ -889,11 +891,12 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       if (lane == 0) {
         mbar_wait_cmp<POLY_CMP_PARK_REC>(&C.rec_empty[r], rph ^ 1u);
         const uint32_t need = (8 * tot + 15) & ~15u, RB = sh.ring_bytes;
-        uint32_t p = (uint32_t)(whead % RB);
+        uint32_t p = hpos;
         if (p + need > RB) {  // wrap: the segment stays contiguous
           whead += RB - p;
           p = 0;
         }
+        hpos = p + need;
         uint32_t ns = 0;
         while (whead + need - C.wtail[warp] > RB) {
           __nanosleep(ns);
@@ -1012,11 +1015,12 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
       TRACE(it, 2);
       mbar_wait_cmp<POLY_CMP_PARK_REC>(&C.rec_empty[r], rph ^ 1u);
       const uint32_t need = (8 * W + 15) & ~15u;
-      uint32_t pos = (uint32_t)(head % sh.ring_bytes);
+      uint32_t pos = hpos;
       if (pos + need > sh.ring_bytes) {
         head += sh.ring_bytes - pos;
         pos = 0;
       }
+      hpos = pos + need;
       uint32_t ns = 0;
       while (head + need - C.ring_tail > sh.ring_bytes) {
         __nanosleep(ns);
@@ -1309,6 +1313,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
     C.ring_tail = 0;
     C.lb_seq = 0;
     C.ring_head = 0;
+    C.ring_hpos = 0;
   }
   cache_fill(bc, true, sh.Le);
   __syncthreads();
@@ -1487,7 +1492,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
           uint64_t a1 = min((hw + 1) & ~1ull, pw & ~1ull);
           if (a1 < a0) a1 = a0;
           const uint32_t need = (uint32_t)((8 * (hw - a0) + 15) & ~15ull);
-          uint32_t pos = (uint32_t)(head % sh.ring_bytes);
+          uint32_t pos = C.ring_hpos;
           if (pos + need > sh.ring_bytes) {  // wrap: the tile's words stay contiguous
             head += sh.ring_bytes - pos;
             pos = 0;
@@ -1505,6 +1510,7 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
           head += need;
           C.ring_end[s] = head;
           C.ring_head = head;
+          C.ring_hpos = pos + need;
           __threadfence_block();
           C.lb_seq = i + 1;
           for (uint64_t w = a1; w < hw; ++w) dst[w - a0] = ldg_nc_u64(pay_g + w);
