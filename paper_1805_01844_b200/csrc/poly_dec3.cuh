@@ -28,7 +28,10 @@
 namespace polyk {
 namespace d3 {
 
-constexpr int NW = 16;                // consumer warps per CTA
+#ifndef POLY_D3_NW
+#define POLY_D3_NW 16
+#endif
+constexpr int NW = POLY_D3_NW;        // consumer warps per CTA
 constexpr int NTHR = 32 * (NW + 1);   // + the producer warp
 constexpr int NSLOT = 16;             // tiles in flight per CTA
 constexpr int TU = 8;                 // units per tile
@@ -642,13 +645,16 @@ __global__ void __launch_bounds__(NTHR, 1) dec3_main(Args a) {
   // -------------------------------------------------------------- consumers
   uint8_t* stg = smem + a.o_warp + (size_t)warp * a.cap;
   uint32_t err = 0;
+  // the next unit is claimed as soon as the current one is known, so the
+  // shared-memory atomic's latency hides behind the decode
+  uint32_t qn = 0;
+  if (lane == 0) qn = atomicAdd(&C.next_unit, 1u);
   for (;;) {
-    uint32_t q = 0;
-    if (lane == 0) q = atomicAdd(&C.next_unit, 1u);
-    q = __shfl_sync(0xffffffffu, q, 0);
+    const uint32_t q = __shfl_sync(0xffffffffu, qn, 0);
     const uint64_t it = q / TU;
     const uint32_t wi = q % TU;
     if (blockIdx.x + it * gridDim.x >= n_tiles) break;
+    if (lane == 0) qn = atomicAdd(&C.next_unit, 1u);
     const uint32_t s = (uint32_t)(it % NSLOT);
     px::mbar_wait(&C.full[s], (uint32_t)(it / NSLOT) & 1u);
     const Slot& S = C.slot[s];

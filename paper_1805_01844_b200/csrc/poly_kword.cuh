@@ -24,6 +24,7 @@
 
 namespace polyk {
 
+
 // min over non-power-of-two B <= 65536 with k(B) = K of t32(B); computed by
 // build_tables() on the host and checked against this table in poly_init.
 __host__ __device__ constexpr int t32min_u16(int K) {
@@ -250,26 +251,24 @@ __device__ __forceinline__ uint32_t unpack_block_k(const uint64_t* src, uint32_t
 // Unpack group g with the base class fixed at compile time (POW2: B = 2^j,
 // digits are bit fields; else binary-fraction steps), so neither path is
 // if-converted into the other (poly_dec3.cuh).
+// Digits of group g into registers r (two values per register); returns
+// status bits.  The group's words are passed in (w), loaded by the caller.
 template <int K, bool POW2>
-__device__ __forceinline__ uint32_t unpack_group_p(const uint64_t* src, uint32_t g, const DecConst& dc, uint32_t B,
-                                                   uint32_t vmin, uint8_t* blk) {
+__device__ __forceinline__ uint32_t unpack_regs_p(const uint64_t (&w)[KCls<K>::Q], const DecConst& dc, uint32_t B,
+                                                  uint32_t vmin, uint32_t (&r)[KCls<K>::NR]) {
   using C = KCls<K>;
   constexpr int T = t32min_u16(K);
-  uint32_t r[C::NR];
   uint32_t err = 0;
   if (POW2) {
-    // B = 2^J with J = 64 / K (the one power-of-two base of capacity K, when
-    // there is one): two J-bit fields per 32-bit register by constant shifts,
-    // vmin added to both halves at once (digit + vmin <= 65535: no carry)
+    // B = 2^J with J = 64 / K (the one power-of-two base of capacity K that
+    // takes this path): two J-bit fields per 32-bit register by constant
+    // shifts, vmin added to both halves at once (digit + vmin <= 65535)
     constexpr int J = 64 / K;
     constexpr uint32_t M = (1u << J) - 1u;
     const uint32_t vmin2 = vmin * 0x10001u;
-    uint64_t w[C::Q];
 #pragma unroll
-    for (int q = 0; q < C::Q; ++q) {
-      w[q] = src[g * C::Q + q];
+    for (int q = 0; q < C::Q; ++q)
       if (K * J < 64 && (w[q] >> (K * J)) != 0) err = POLY_ST_RESIDUE;
-    }
 #pragma unroll
     for (int p = 0; p < C::NR; ++p) {
       const int q0 = (2 * p) / K, e0 = (2 * p) % K, q1 = (2 * p + 1) / K, e1 = (2 * p + 1) % K;
@@ -286,7 +285,7 @@ __device__ __forceinline__ uint32_t unpack_group_p(const uint64_t* src, uint32_t
   } else {
 #pragma unroll
     for (int q = 0; q < C::Q; ++q) {
-      const uint64_t s = src[g * C::Q + q];
+      const uint64_t s = w[q];
       const int o = q * K;
       uint32_t d[K];
       if (s > dc.Wmax) err = POLY_ST_RESIDUE;
@@ -321,6 +320,17 @@ __device__ __forceinline__ uint32_t unpack_group_p(const uint64_t* src, uint32_t
       }
     }
   }
+  return err;
+}
+template <int K, bool POW2>
+__device__ __forceinline__ uint32_t unpack_group_p(const uint64_t* src, uint32_t g, const DecConst& dc, uint32_t B,
+                                                   uint32_t vmin, uint8_t* blk) {
+  using C = KCls<K>;
+  uint64_t w[C::Q];
+  uint32_t r[C::NR];
+#pragma unroll
+  for (int q = 0; q < C::Q; ++q) w[q] = src[g * C::Q + q];
+  const uint32_t err = unpack_regs_p<K, POW2>(w, dc, B, vmin, r);
   store_group<K>(blk + (size_t)g * C::BYTES, r);
   return err;
 }
