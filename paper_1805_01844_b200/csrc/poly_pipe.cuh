@@ -985,7 +985,9 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
           C.smax[seg] = mx;
         }
       }
+      if (ctid == 0) TRACE(it, 9);
       cons_bar<NW>();
+      if (ctid == 0) TRACE(it, 11);
       // per-block reduction of the segments and the in-tile word offsets: by
       // warp 0 alone when the tile has at most 32 blocks (no CTA scan, the
       // other warps go straight to the barrier before the pack)

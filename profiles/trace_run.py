@@ -17,7 +17,8 @@ from paper_1805_01844_b200 import polycomp as pc  # noqa: E402
 import workloads  # noqa: E402
 
 TILES, EV = 1024, 16
-NAMES_C = {0: "ticket", 1: "in landed(w0)", 2: "AGG published", 3: "ring alloc", 4: "pack done(w0)",
+NAMES_C = {0: "ticket", 1: "in landed(w0)", 9: "minmax done(w0)", 11: "barrier 1 passed", 2: "AGG published",
+           3: "ring alloc", 4: "pack done(w0)",
            8: "pack done(w15)", 5: "writer got rec", 6: "lookback done", 7: "copy done"}
 NAMES_D = {0: "ticket", 1: "hdr landed", 2: "AGG published", 3: "LB start", 4: "lookback done", 5: "ring alloc",
            6: "payload landed(w0)", 9: "payload landed(w15)", 7: "w0 done", 8: "last warp done"}
@@ -50,6 +51,17 @@ def report(tr, names, label, pairs):
             per.append(np.median(np.diff(ts[n // 4: 3 * n // 4])) / 1000.0)
     if per:
         print("  tile period per CTA (ticket to ticket): med %.2f us" % np.median(per))
+    # warp 0: from its pack end to the next tile's stage landing (input wait)
+    if valid[:, :, 4].any() and valid[:, :, 1].any():
+        g = []
+        for c in range(tr.shape[0]):
+            n = int(ok[c].sum())
+            if n > 8:
+                a4 = tr[c, n // 4: 3 * n // 4, 4].astype(np.int64)
+                b1 = tr[c, n // 4 + 1: 3 * n // 4 + 1, 1].astype(np.int64)
+                g.append(np.median(b1 - a4) / 1000.0)
+        if g:
+            print("  pack done(w0) -> next in landed(w0): med %.2f us" % np.median(g))
     end = max(int(tr[:, :, e][valid[:, :, e]].max()) for e in names if valid[:, :, e].any())
     print("  span first ticket -> last event: %.1f us" % ((end - int(t0)) / 1000.0))
 
@@ -85,8 +97,10 @@ def main():
         ok = tr[:, :, 0] != np.uint64(0xffffffffffffffff)
         nc, nt = int(ok.any(1).sum()), int(ok.sum(1).max())
         np.savez_compressed(args.out + "_%s.npz" % tag, tr=tr[:max(nc, 1), :max(nt, 1)])
-    report(tc, NAMES_C, "compress", [(0, 1), (1, 2), (2, 3), (3, 4), (4, 8), (4, 5), (5, 6), (6, 7), (0, 7)])
-    report(td, NAMES_D, "decompress", [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (5, 6), (6, 9), (6, 7), (7, 8), (0, 8)])
+    report(tc, NAMES_C, "compress", [(0, 1), (1, 9), (9, 11), (11, 2), (2, 3), (3, 4), (4, 8), (4, 5), (5, 6), (6, 7),
+                                     (0, 7)])
+    if (td[:, :, 0] != np.uint64(0xffffffffffffffff)).any():  # pipeline decompress (map 0) only
+        report(td, NAMES_D, "decompress", [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (5, 6), (6, 9), (6, 7), (7, 8), (0, 8)])
 
 
 if __name__ == "__main__":
