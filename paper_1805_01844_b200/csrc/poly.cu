@@ -559,9 +559,12 @@ bool plan_dec3(const Shape& sh, Dec3Plan& P) {
   a.n_chunks = (sh.n_blocks + d3::CE - 1) / d3::CE;
   const uint32_t kmin = 1u << a.kmin_log2;
   a.max_units = (sh.n_blocks - 1) * dec3_units_max(sh.Le, a.ut, kmin) + dec3_units_max(a.last_len, a.ut, kmin);
-  a.cap = (uint32_t)((a.ut * a.vb + 32 + 15) / 16 * 16);
+  // a staging buffer holds a unit of up to capv values (unit_words) plus the
+  // 16-byte alignment shift of the generic path; two per warp (TMA stores)
+  a.capv = a.ut + 128u;
+  a.cap = (uint32_t)((a.capv * a.vb + 32 + 15) / 16 * 16);
   a.o_warp = (uint32_t)((sizeof(d3::Ctl) + 127) / 128 * 128);
-  a.o_ring = (a.o_warp + d3::NW * a.cap + 127) / 128 * 128;
+  a.o_ring = (a.o_warp + d3::NW * 2 * a.cap + 127) / 128 * 128;
   const uint32_t smax = 227 * 1024;
   a.ring_bytes = (smax - a.o_ring) / 16 * 16;
   // worst tile: TU units of <= ut / k_min + 8 words, their headers, the table entries
@@ -827,6 +830,18 @@ int poly_trace_dump(void* host, uint64_t bytes) {
   return cudaMemcpyFromSymbol(host, polyk::g_trace, bytes) == cudaSuccess ? 0 : 1;
 }
 uint64_t poly_trace_bytes(void) { return sizeof(polyk::g_trace); }
+#endif
+
+#ifdef POLY_PROBE
+// Timing experiments only (not in include/poly.h): dec3 cycle counters.
+int poly_probe_reset(void) {
+  void* p = nullptr;
+  if (cudaGetSymbolAddress(&p, polyk::d3::g_probe) != cudaSuccess) return 1;
+  return cudaMemset(p, 0, sizeof(polyk::d3::g_probe)) == cudaSuccess ? 0 : 1;
+}
+int poly_probe_dump(void* host) {
+  return cudaMemcpyFromSymbol(host, polyk::d3::g_probe, sizeof(polyk::d3::g_probe)) == cudaSuccess ? 0 : 1;
+}
 #endif
 
 int poly_launches_per_call(uint64_t n, poly_dtype_t dt, uint64_t block_size, int decompress) {

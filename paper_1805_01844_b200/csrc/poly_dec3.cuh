@@ -14,8 +14,9 @@
 //    cross-CTA dependency: a producer warp per CTA bulk-loads (TMA) tiles of
 //    TU units -- table entries, block headers, payload words -- up to NSLOT
 //    tiles ahead; consumer warps claim units one at a time and decode each
-//    into their own staging buffer, which they copy to HBM themselves with
-//    16-byte stores (no shared staging tile waits for a bulk store).  u16
+//    into one of their two staging buffers, which a TMA bulk store of the
+//    warp copies to HBM while the warp decodes the next unit into the other.
+//    Units split a block into equal parts of about UT values.  u16
 //    blocks that start 16-byte aligned use the k-specialised, bank-conflict-
 //    free group codec of poly_kword.cuh (unit boundaries fall on multiples of
 //    8 words, so every group is 16-byte aligned in the staging buffer); other
@@ -34,9 +35,27 @@ namespace d3 {
 constexpr int NW = POLY_D3_NW;        // consumer warps per CTA
 constexpr int NTHR = 32 * (NW + 1);   // + the producer warp
 constexpr int NSLOT = 16;             // tiles in flight per CTA
-constexpr int TU = 8;                 // units per tile
+constexpr int TU = 8;                 // units per tile (16: the ring no longer holds two worst-case tiles)
+constexpr int PFD = 4;                // producer: unit-table prefetch depth (tiles)
 constexpr uint32_t CE = 2048;         // pass 1: blocks per chunk
 constexpr int K1T = 256;              // pass 1 threads per CTA
+
+// POLY_PROBE (timing experiments only, a separate library variant): cycle
+// counters per role, summed over warps (lane 0's clock64).
+#ifdef POLY_PROBE
+__device__ unsigned long long g_probe[16];
+#define PROBE_DECL long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}
+#define PROBE_T0(v) const long long v = clock64()
+#define PROBE_ADD(i, t0) pacc[i] += clock64() - (t0)
+#define PROBE_FLUSH                                                                  \
+  if ((threadIdx.x & 31) == 0)                                                       \
+    for (int i_ = 0; i_ < 8; ++i_) atomicAdd(&g_probe[i_], (unsigned long long)pacc[i_])
+#else
+#define PROBE_DECL
+#define PROBE_T0(v)
+#define PROBE_ADD(i, t0)
+#define PROBE_FLUSH
+#endif
 
 struct Args {
   const uint8_t* in;
@@ -53,7 +72,8 @@ struct Args {
   uint32_t block_len, width, vb, kmin_log2;
   uint32_t ut;           // values per unit (target)
   uint32_t kw_ok;        // u16 blocks start 16-byte aligned in the output: k-specialised codec
-  uint32_t cap;          // staging bytes per warp
+  uint32_t capv;         // values a unit may hold (the staging buffer's capacity)
+  uint32_t cap;          // bytes per staging buffer (two per warp)
   uint32_t o_warp, o_ring, ring_bytes;
 };
 
@@ -64,6 +84,18 @@ __device__ __forceinline__ uint32_t wpu_of(uint32_t ut, uint32_t k) {
   return w < 8 ? 8u : w;
 }
 
+
+// Words per unit of a valid BASIC block (capacity k, nw words): the whole
+// block when its words fit a staging buffer (nw k <= capv values); else the
+// fewest units of about ut values, as equal as a multiple of 8 words allows,
+// when they fit; else WPU(k).  Passes 1 and 2 agree through the unit table.
+__device__ __forceinline__ uint32_t unit_words(uint32_t ut, uint32_t capv, uint32_t k, uint32_t nw) {
+  if ((uint64_t)nw * k <= capv) return (nw + 7) & ~7u;
+  const uint32_t nu = (uint32_t)(((uint64_t)(nw - 1) * k + ut - 1) / ut);
+  const uint32_t w = ((nw + nu - 1) / nu + 7) & ~7u;
+  if ((uint64_t)w * k <= capv) return w;
+  return wpu_of(ut, k);
+}
 
 // ------------------------------------------------------------------ checks
 // Global header against the call's arguments (a9).  The
@@ -314,20 +346,20 @@ __device__ __forceinline__ uint32_t dec_word_dc(uint64_t s, const DecConst& dc, 
 }
 
 // ------------------------------------------------------------------ output
-// Copy the global byte range [c_lo, c_hi) from the staging buffer, whose byte
-// x holds global byte G0 + x (G0 16-byte aligned): 16-byte stores inside,
-// element stores for the partial 16-byte chunks at the ends (a neighbouring
-// round or warp writes the rest of those chunks).
+// Store the global byte range [c_lo, c_hi) from the staging buffer, whose
+// byte x holds global byte G0 + x (G0 16-byte aligned): one TMA bulk store of
+// the 16-byte aligned interior
+// (issued by lane 0 into the warp's current bulk group; the caller commits
+// and waits) and element stores for the partial chunks at the ends.  Every
+// lane's staging writes are made visible to the async proxy first.
 template <typename V>
-__device__ __forceinline__ void copy_out(const uint8_t* stg, uint64_t G0, uint64_t c_lo, uint64_t c_hi, int lane) {
+__device__ __forceinline__ void store_out(const uint8_t* stg, uint64_t G0, uint64_t c_lo, uint64_t c_hi, int lane) {
   if (c_lo >= c_hi) return;
   const uint64_t a16 = (c_lo + 15) & ~15ull, b16 = c_hi & ~15ull;
   if (a16 < b16) {
-    const uint32_t nch = (uint32_t)((b16 - a16) >> 4);
-    const uint8_t* src = stg + (a16 - G0);
-#pragma unroll 2
-    for (uint32_t q = lane; q < nch; q += 32)
-      px::st_v4(reinterpret_cast<void*>(a16 + 16ull * q), *reinterpret_cast<const uint4*>(src + 16 * q));
+    px::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) px::bulk_s2g(reinterpret_cast<void*>(a16), stg + (a16 - G0), (uint32_t)(b16 - a16));
     const uint32_t nh = (uint32_t)(a16 - c_lo) / sizeof(V), nt = (uint32_t)(c_hi - b16) / sizeof(V);
     if ((uint32_t)lane < nh) {
       reinterpret_cast<V*>(c_lo)[lane] = reinterpret_cast<const V*>(stg + (c_lo - G0))[lane];
@@ -405,7 +437,7 @@ __device__ __forceinline__ uint32_t units_of(const Args& a, uint4 h, uint32_t bl
   if (h.x == CODEC_BASIC && h.z != 0 && (uint64_t)h.y + h.z <= vmax) {
     const uint32_t k = capacity_of((uint64_t)h.z + 1);
     if (h.w != 0 && (uint64_t)(h.w - 1) * k < blen && (uint64_t)h.w * k >= blen) {
-      const uint32_t w = wpu_of(a.ut, k);
+      const uint32_t w = unit_words(a.ut, a.capv, k, h.w);
       return (h.w + w - 1) / w;
     }
   }
@@ -509,9 +541,9 @@ __global__ void __launch_bounds__(K1T) dec3_offsets(Args a) {
         const uint4 h = px::ld_v4(H + b0 + i);
         const uint32_t blen = block_len_of(a, b0 + i);
         uint32_t w = 0;
-        if (nu > 1 || (h.x == CODEC_BASIC && h.z != 0)) {
+        if (nu > 1) {  // a valid BASIC block (units_of)
           const uint32_t k = capacity_of((uint64_t)h.z + 1);
-          w = wpu_of(a.ut, k);
+          w = unit_words(a.ut, a.capv, k, h.w);
         }
         (void)blen;
         const uint64_t u0 = Pu + s_u[i], ws = Pw + s_w[i];
@@ -543,7 +575,6 @@ __global__ void __launch_bounds__(K1T) dec3_offsets(Args a) {
 struct Slot {
   uint64_t ws;    // first payload word loaded
   uint64_t we;    // payload word after the tile's last unit
-  uint64_t u0;    // first unit
   uint64_t hb0;   // first block whose header is staged
   uint32_t off_t, off_h, off_p;  // ring byte offsets: table entries, headers, payload word ws
   uint32_t nu;
@@ -582,13 +613,44 @@ __global__ void __launch_bounds__(NTHR, 1) dec3_main(Args a) {
 
   if (warp == NW) {
     // ------------------------------------------------------------ producer
+    // The unit-table entries that bound each tile (first unit, last unit,
+    // the unit after) are loaded PFD tiles ahead (a register queue), so their
+    // latency overlaps the waits and copies of the tiles before.
     if (lane != 0) return;
-    const uint64_t RB = a.ring_bytes;
+    PROBE_DECL;
+    PROBE_T0(pt0);
+    const uint32_t RB = a.ring_bytes;
     uint64_t head = 0, tail = 0, rc = 0, it = 0;
+    uint32_t hpos = 0;
+    uint4 q0[PFD], ql[PFD], qn[PFD];
+#pragma unroll
+    for (int i = 0; i < PFD; ++i) {
+      const uint64_t tl = blockIdx.x + (uint64_t)i * gridDim.x;
+      q0[i] = ql[i] = qn[i] = make_uint4(0, 0, 0, 0);
+      if (tl < n_tiles) {
+        const uint64_t v0 = tl * TU, v1 = min(v0 + TU, U);
+        q0[i] = px::ld_v4(a.T + v0);
+        ql[i] = px::ld_v4(a.T + v1 - 1);
+        qn[i] = px::ld_v4(a.T + v1);
+      }
+    }
     for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+      const uint4 e0 = q0[0], el = ql[0], en = qn[0];
+#pragma unroll
+      for (int i = 0; i + 1 < PFD; ++i) {
+        q0[i] = q0[i + 1];
+        ql[i] = ql[i + 1];
+        qn[i] = qn[i + 1];
+      }
+      const uint64_t tn = t + (uint64_t)PFD * gridDim.x;
+      if (tn < n_tiles) {
+        const uint64_t v0 = tn * TU, v1 = min(v0 + TU, U);
+        q0[PFD - 1] = px::ld_v4(a.T + v0);
+        ql[PFD - 1] = px::ld_v4(a.T + v1 - 1);
+        qn[PFD - 1] = px::ld_v4(a.T + v1);
+      }
       const uint64_t u0 = t * TU, u1 = min(u0 + TU, U);
       const uint32_t nu = (uint32_t)(u1 - u0);
-      const uint4 e0 = a.T[u0], el = a.T[u1 - 1], en = a.T[u1];
       const uint64_t ws = ws_of(e0), we = ws_of(en);
       const uint64_t hb0 = e0.x, hb1 = (uint64_t)el.x + 1;
       const uint64_t pa = pay_byte0 + 8 * ws, pe = pay_byte0 + 8 * we;
@@ -602,33 +664,35 @@ __global__ void __launch_bounds__(NTHR, 1) dec3_main(Args a) {
       const uint32_t bt = 16 * nu, bh = (uint32_t)(16 * (hb1 - hb0));
       const uint32_t bp = (uint32_t)(pe16 - pa16) + 16 * tailw;
       const uint32_t need = bt + bh + bp;
+      PROBE_T0(pw0);
       while (it - rc >= NSLOT) {
         const uint32_t s = (uint32_t)(rc % NSLOT);
         px::mbar_wait(&C.empty[s], (uint32_t)(rc / NSLOT) & 1u);
         tail = C.send[s];
         ++rc;
       }
-      uint64_t pos = head % RB;
+      uint32_t pos = hpos;  // head modulo the ring size, kept incrementally
       if (pos + need > RB) {
         head += RB - pos;
         pos = 0;
       }
+      hpos = pos + need;
       while (head + need - tail > RB) {
         const uint32_t s = (uint32_t)(rc % NSLOT);
         px::mbar_wait(&C.empty[s], (uint32_t)(rc / NSLOT) & 1u);
         tail = C.send[s];
         ++rc;
       }
+      PROBE_ADD(5, pw0);
       const uint32_t s = (uint32_t)(it % NSLOT);
       Slot& S = C.slot[s];
       S.ws = ws;
       S.we = we;
-      S.u0 = u0;
       S.hb0 = hb0;
       S.nu = nu;
-      S.off_t = (uint32_t)pos;
-      S.off_h = (uint32_t)pos + bt;
-      S.off_p = (uint32_t)pos + bt + bh + (uint32_t)(pa - pa16);
+      S.off_t = pos;
+      S.off_h = pos + bt;
+      S.off_p = pos + bt + bh + (uint32_t)(pa - pa16);
       head += need;
       C.send[s] = head;
       uint8_t* dst = ring + pos;
@@ -639,15 +703,22 @@ __global__ void __launch_bounds__(NTHR, 1) dec3_main(Args a) {
       px::bulk_g2s(dst + bt, a.in + 32 + 16 * hb0, bh, &C.full[s]);
       if (pe16 > pa16) px::bulk_g2s(dst + bt + bh, a.in + pa16, (uint32_t)(pe16 - pa16), &C.full[s]);
     }
+    PROBE_ADD(4, pt0);
+    PROBE_FLUSH;
     return;
   }
 
   // -------------------------------------------------------------- consumers
-  uint8_t* stg = smem + a.o_warp + (size_t)warp * a.cap;
+  // two staging buffers per warp: a unit is decoded into one while the TMA
+  // store of the previous unit reads the other
+  uint8_t* const stg2 = smem + a.o_warp + (size_t)warp * 2 * a.cap;
+  uint32_t bi = 0;
   uint32_t err = 0;
   // the next unit is claimed as soon as the current one is known, so the
   // shared-memory atomic's latency hides behind the decode
   uint32_t qn = 0;
+  PROBE_DECL;
+  PROBE_T0(ct0);
   if (lane == 0) qn = atomicAdd(&C.next_unit, 1u);
   for (;;) {
     const uint32_t q = __shfl_sync(0xffffffffu, qn, 0);
@@ -656,8 +727,15 @@ __global__ void __launch_bounds__(NTHR, 1) dec3_main(Args a) {
     if (blockIdx.x + it * gridDim.x >= n_tiles) break;
     if (lane == 0) qn = atomicAdd(&C.next_unit, 1u);
     const uint32_t s = (uint32_t)(it % NSLOT);
+    PROBE_T0(cw0);
     px::mbar_wait(&C.full[s], (uint32_t)(it / NSLOT) & 1u);
+    PROBE_ADD(1, cw0);
+    PROBE_T0(cd0);
     const Slot& S = C.slot[s];
+    uint8_t* const stg = stg2 + bi * a.cap;
+    bi ^= 1u;
+    if (lane == 0) px::bulk_wait_read<1>();  // this buffer's previous store has read it
+    __syncwarp();
     if (wi < S.nu) {
       const uint4* TE = reinterpret_cast<const uint4*>(ring + S.off_t);
       const uint4 e = TE[wi];
@@ -710,7 +788,10 @@ __global__ void __launch_bounds__(NTHR, 1) dec3_main(Args a) {
           }
           __syncwarp();
           const uint32_t nv = min(blen, j1 * k) - j0 * k;
-          copy_out<V>(stg, gbase, gbase, gbase + (uint64_t)nv * 2, lane);
+          PROBE_ADD(2, cd0);
+          PROBE_T0(cc0);
+          store_out<V>(stg, gbase, gbase, gbase + (uint64_t)nv * 2, lane);
+          PROBE_ADD(3, cc0);
         }
       }
       if (!fast) {
@@ -731,13 +812,22 @@ __global__ void __launch_bounds__(NTHR, 1) dec3_main(Args a) {
           }
           __syncwarp();
           const uint32_t nv = (uint32_t)min((uint64_t)blen, (uint64_t)j1 * k) - j0 * k;
-          copy_out<V>(stg, G0, gbase, gbase + (uint64_t)nv * sizeof(V), lane);
+          store_out<V>(stg, G0, gbase, gbase + (uint64_t)nv * sizeof(V), lane);
         }
       }
     }
     __syncwarp();
-    if (lane == 0) px::mbar_arrive(&C.empty[s]);
+    if (lane == 0) {
+      px::mbar_arrive(&C.empty[s]);
+      px::bulk_commit();  // one bulk group per unit (possibly empty)
+    }
+#ifdef POLY_PROBE
+    pacc[7] += 1;
+#endif
   }
+  PROBE_ADD(0, ct0);
+  PROBE_FLUSH;
+  if (lane == 0) px::bulk_wait_all<0>();  // the stores have read the staging (and landed)
   err = __reduce_or_sync(0xffffffffu, err);
   if (lane == 0 && err) atomicOr(a.status_out, err);
 }
