@@ -13,6 +13,7 @@
 #include "poly_large.cuh"
 #include "poly_adv.cuh"
 #include "poly_dec3.cuh"
+#include "poly_cmp3.cuh"
 
 #include <vector>
 
@@ -312,6 +313,8 @@ void set_attrs(int pmax) {
   set_smem_attr(poly_decompress_large1<V>, large_smem_unpack<V>());
   set_smem_attr(poly_compress_large1<V>, large_smem_pack<V>());
   set_smem_attr(d3::dec3_main<V>, 227 * 1024);
+  set_smem_attr(c3::cmp3<V, false>, 227 * 1024);
+  set_smem_attr(c3::cmp3<V, true>, 227 * 1024);
 }
 
 poly_status_t ensure_init(int dev) {
@@ -438,8 +441,46 @@ bool plan_pipe_n(const Shape& sh, PipeShape& ps, bool decomp, uint32_t ncw) {
 // larger block parts (fewer warps per block: fewer group barriers and part
 // tails), ties to the larger warp count (measured: cfg5 12 warps / 4 KiB
 // parts 1751 GB/s vs 16 / 2 KiB 1439; cfg4 16 warps).
+// Compress of blocks whose byte size is a multiple of 16 (poly_cmp3.cuh):
+// tiles of about C3_TILE bytes in S slots, S a multiple of the writer count.
+bool plan_c3(const Shape& sh, PipeShape& ps) {
+  memset(&ps, 0, sizeof ps);
+  const uint64_t bb = sh.Le * (sh.width / 8);
+  if (bb <= MAP0_MAX_BLOCK || bb > PIPE_MAX_BLOCK || bb % 16 != 0) return false;
+  ps.c3 = 1;
+  ps.map = 1;
+  ps.ncw = c3::NW;
+  ps.n = sh.n;
+  ps.Le = sh.Le;
+  ps.n_blocks = sh.n_blocks;
+  ps.block_len = sh.block_len;
+  ps.width = sh.width;
+  ps.vb = sh.width / 8;
+  ps.TB = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(c3::TBMAX, c3::C3_TILE / bb));
+  // G = blocks per consumer claim: a power of two <= 32 with about 8 KiB of
+  // values per claim (small blocks share one claim's overheads), TB a multiple
+  uint32_t cb = 1;
+  while (cb < 32 && 2ull * cb * bb <= c3::C3_CLAIM && 2 * cb <= ps.TB) cb *= 2;
+  ps.G = cb;
+  ps.TB = ps.TB / cb * cb;
+  ps.tile_bytes = (uint32_t)(ps.TB * bb);
+  ps.words_cap = (uint32_t)(ps.TB * ((sh.Le + kmin_of(sh.width) - 1) / kmin_of(sh.width)));
+  ps.n_tiles = (sh.n_blocks + ps.TB - 1) / ps.TB;
+  if (ps.n_tiles >= (1ull << 32)) return false;
+  ps.o_cache = (uint32_t)((sizeof(c3::Ctl) + 127) / 128 * 128);
+  ps.o_in = (ps.o_cache + cache_bytes(false) + 127) / 128 * 128;
+  ps.in_stride = (ps.tile_bytes + 127) / 128 * 128;
+  uint32_t S = std::min<uint32_t>(c3::MAXS3, (PIPE_SMEM_MAX - ps.o_in) / ps.in_stride);
+  S = S / c3::NWR * c3::NWR;
+  if (S < (uint32_t)c3::NWR || S < 2) return false;
+  ps.S = S;
+  ps.smem = ps.o_in + S * ps.in_stride;
+  return true;
+}
+
 bool plan_pipe(const Shape& sh, PipeShape& ps, bool decomp) {
   const bool map0 = (uint64_t)sh.Le * (sh.width / 8) <= MAP0_MAX_BLOCK;
+  if (!decomp && !map0 && plan_c3(sh, ps)) return true;
   if (!decomp) {
     // map 1: NCW_C2 warps when NCW_C would split each block over 4 or more
     // warps and the smaller count keeps the tile (measured, cfg5: 24 warps /
@@ -702,6 +743,15 @@ void launch_compress_pipe(const Shape& sh, poly_dtype_t dt, const void* d_in, ui
   // to the writers: 4 of them keep up (measured: 2 -> 1254, 4 -> 2078 GB/s cfg2)
   const bool wr = pa.sh.wrings != 0;
   pa.nlb = lb_warps(wr ? 4 : 2, NLB_MAX + 1);
+  if (pa.sh.c3) {
+    pa.nlb = c3::NWR;
+    POLY_DISPATCH(dt, {
+      auto k = pa.sh.G > 1 ? c3::cmp3<V, true> : c3::cmp3<V, false>;
+      const int grid = pipe_grid_server(k, c3::NTHR, pa.sh.smem, pa.t_end - pa.t_begin, dev, pa.server);
+      launch_k(k, grid, c3::NTHR, pa.sh.smem, s, pa.server != 0, pa);
+    });
+    return;
+  }
   POLY_DISPATCH(dt, {
     auto k = pa.sh.map == 0         ? poly_compress_pipe<V, 0, NCW_C>
              : pa.sh.ncw == NCW_C ? poly_compress_pipe<V, 1, NCW_C>
@@ -839,7 +889,7 @@ int poly_probe_reset(void) {
   if (cudaGetSymbolAddress(&p, polyk::d3::g_probe) != cudaSuccess) return 1;
   return cudaMemset(p, 0, sizeof(polyk::d3::g_probe)) == cudaSuccess ? 0 : 1;
 }
-int poly_probe_dump(void* host) {
+int poly_probe_dump(void* host) {  // 24 u64
   return cudaMemcpyFromSymbol(host, polyk::d3::g_probe, sizeof(polyk::d3::g_probe)) == cudaSuccess ? 0 : 1;
 }
 #endif

@@ -43,13 +43,14 @@ constexpr int K1T = 256;              // pass 1 threads per CTA
 // POLY_PROBE (timing experiments only, a separate library variant): cycle
 // counters per role, summed over warps (lane 0's clock64).
 #ifdef POLY_PROBE
-__device__ unsigned long long g_probe[16];
-#define PROBE_DECL long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}
+__device__ unsigned long long g_probe[24];
+#define PROBE_DECL long long pacc[24] = {}
 #define PROBE_T0(v) const long long v = clock64()
 #define PROBE_ADD(i, t0) pacc[i] += clock64() - (t0)
 #define PROBE_FLUSH                                                                  \
   if ((threadIdx.x & 31) == 0)                                                       \
-    for (int i_ = 0; i_ < 8; ++i_) atomicAdd(&g_probe[i_], (unsigned long long)pacc[i_])
+    for (int i_ = 0; i_ < 24; ++i_)                                                  \
+      if (pacc[i_]) atomicAdd(&g_probe[i_], (unsigned long long)pacc[i_])
 #else
 #define PROBE_DECL
 #define PROBE_T0(v)

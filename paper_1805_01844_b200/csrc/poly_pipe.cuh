@@ -107,6 +107,7 @@ struct PipeShape {
   uint32_t nslot;       // compress: records in flight (<= MAXR)
   uint32_t slot_bytes;  // compress: bytes of each consumer warp's word ring
   uint32_t ncw;         // consumer warps of the kernel instantiation this shape is for
+  uint32_t c3;          // compress: the in-place one-warp-per-block kernel (poly_cmp3.cuh)
   uint32_t smem;        // dynamic shared memory bytes
 };
 
@@ -568,7 +569,11 @@ __device__ __forceinline__ void warp_copy(uint8_t* dst, const uint8_t* src, uint
 // per read.  Its SM carries no bulk traffic, so its reads return quickly; a
 // worker then needs one word, status[t - 1], to learn its tile's offset
 // instead of walking back through other tiles.
+// PER tiles per lane per read (32 PER per round; measured for the 24 KiB
+// tiles of cmp3: 8 and 16 alike).
+template <int PER = LB_PER>
 __device__ __noinline__ void prefix_server(uint64_t* status, uint64_t n_tiles, uint64_t t_begin = 0) {
+  constexpr int LB_PER = PER;
   // tiles [t_begin, n_tiles); a range after the first continues from the
   // inclusive prefix the previous launch's server left in status[t_begin - 1]
   const int lane = threadIdx.x & 31;
@@ -594,24 +599,25 @@ __device__ __noinline__ void prefix_server(uint64_t* status, uint64_t n_tiles, u
       continue;
     }
     ns = 0;
-    // inclusive prefixes of the run [f, f + q)
-    uint64_t loc[LB_PER], run = 0;
+    // inclusive prefixes of the run [f, f + q) (the lane's running sum is
+    // recomputed while storing, so only e[] stays in registers)
+    uint64_t run = 0;
 #pragma unroll
-    for (int j = 0; j < LB_PER; ++j) {
+    for (int j = 0; j < LB_PER; ++j)
       if ((uint32_t)(LB_PER * lane + j) < q) run += e[j] & VAL_MASK;
-      loc[j] = run;
-    }
     uint64_t inc = run;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint64_t y = __shfl_up_sync(0xffffffffu, inc, o);
       if (lane >= o) inc += y;
     }
-    const uint64_t excl = P + inc - run;
+    uint64_t acc = P + inc - run;
 #pragma unroll
     for (int j = 0; j < LB_PER; ++j)
-      if ((uint32_t)(LB_PER * lane + j) < q)
-        st_relaxed_u64(status + f + LB_PER * lane + j, FLAG_PRE | ((excl + loc[j]) & VAL_MASK));
+      if ((uint32_t)(LB_PER * lane + j) < q) {
+        acc += e[j] & VAL_MASK;
+        st_relaxed_u64(status + f + LB_PER * lane + j, FLAG_PRE | (acc & VAL_MASK));
+      }
     P += __shfl_sync(0xffffffffu, inc, 31);
     f += q;
   }
