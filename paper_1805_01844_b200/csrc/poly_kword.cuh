@@ -334,11 +334,33 @@ __device__ __forceinline__ uint32_t unpack_group_p(const uint64_t* src, uint32_t
   store_group<K>(blk + (size_t)g * C::BYTES, r);
   return err;
 }
+#ifndef POLY_KP_PAIR
+#define POLY_KP_PAIR 0
+#endif
 template <int K, bool POW2>
 __device__ __forceinline__ uint32_t unpack_groups_kp(const uint64_t* src, uint32_t gb, uint32_t ge, const DecConst& dc,
                                                      uint32_t B, uint32_t vmin, uint8_t* blk) {
   uint32_t err = 0;
-  for (uint32_t g = gb + (threadIdx.x & 31); g < ge; g += 32) err |= unpack_group_p<K, POW2>(src, g, dc, B, vmin, blk);
+  uint32_t g = gb + (threadIdx.x & 31);
+#if POLY_KP_PAIR
+  // two groups per lane per step (independent multiply chains), the second
+  // one clamped to a valid group and not stored when past the end
+  using C = KCls<K>;
+  for (; g + 32 < ge; g += 64) {
+    uint64_t w0[C::Q], w1[C::Q];
+    uint32_t r0[C::NR], r1[C::NR];
+#pragma unroll
+    for (int q = 0; q < C::Q; ++q) {
+      w0[q] = src[g * C::Q + q];
+      w1[q] = src[(g + 32) * C::Q + q];
+    }
+    err |= unpack_regs_p<K, POW2>(w0, dc, B, vmin, r0);
+    err |= unpack_regs_p<K, POW2>(w1, dc, B, vmin, r1);
+    store_group<K>(blk + (size_t)g * C::BYTES, r0);
+    store_group<K>(blk + (size_t)(g + 32) * C::BYTES, r1);
+  }
+#endif
+  for (; g < ge; g += 32) err |= unpack_group_p<K, POW2>(src, g, dc, B, vmin, blk);
   return err;
 }
 

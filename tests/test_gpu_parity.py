@@ -386,3 +386,47 @@ def test_graph_capture_replay(oracle_lib, cfg):
         ref = oracle_lib.compress(xs.cpu().numpy(), L)
         assert out[:nbytes0].cpu().numpy().tobytes() == ref
         assert int(st.item()) == 0 and torch.equal(y, xs)
+
+
+# ------------------------------------------------------------------ in-place compress (poly_cmp3.cuh)
+# Blocks whose byte size is a multiple of 16 (128 B < block <= 32 KiB) are
+# packed in place by one warp per block; small blocks are claimed several at a
+# time (32 / CB lanes per block in the min / max).  Both instantiations, every
+# capacity's threshold bases with their worst words, u32 with B = 2^32, ragged
+# last blocks.
+def _threshold_bases():
+    Bs = set()
+    for k in range(4, 65):
+        # around the first B whose capacity drops below k (coarse steps above 64)
+        b = 2
+        while b <= 65536 and capacity_u64(b) >= k:
+            b += max(1, b // 64)
+        for c in (b - 2, b - 1, b, b + 1):
+            if 2 <= c <= 65536:
+                Bs.add(c)
+    return sorted(Bs | {2, 3, 4, 5, 16, 17, 255, 256, 257, 4096, 7131, 7132, 7133, 65535, 65536})
+
+
+@pytest.mark.parametrize("L", [4096, 1024, 128, 8000])
+def test_inplace_compress_u16_threshold_bases(oracle_lib, L):
+    rng = np.random.default_rng(L)
+    Bs = _threshold_bases()
+    x = worst_case_blocks(Bs, L, rng)
+    check_case(oracle_lib, x, L)
+    check_case(oracle_lib, x[: x.size - L // 3], L)  # a ragged last block
+
+
+def test_inplace_compress_u32(oracle_lib):
+    rng = np.random.default_rng(31)
+    for L in (64, 1024, 4096):
+        blocks = []
+        for B in [2, 3, 65536, 65537, 2642245, 2642246, (1 << 31) + 11, (1 << 32) - 1, 1 << 32]:
+            blk = rng.integers(0, B, size=L, dtype=np.uint64)
+            k = capacity_u64(B)
+            blk[0], blk[1] = 0, B - 1
+            blk[L - (L % k or k):] = B - 1
+            blocks.append(blk)
+        blocks.append(np.full(L, 7, dtype=np.uint64))  # constant block
+        x = np.concatenate(blocks * 3).astype(np.uint32)
+        check_case(oracle_lib, x, L)
+        check_case(oracle_lib, x[:-5], L)
