@@ -601,9 +601,11 @@ bool plan_dec3(const Shape& sh, Dec3Plan& P) {
   const uint32_t kmin = 1u << a.kmin_log2;
   a.max_units = (sh.n_blocks - 1) * dec3_units_max(sh.Le, a.ut, kmin) + dec3_units_max(a.last_len, a.ut, kmin);
   // a staging buffer holds a unit of up to capv values (unit_words) plus the
-  // 16-byte alignment shift of the generic path; two per warp (TMA stores)
+  // 16-byte alignment shift of the generic path and the group codec's overhang
+  // past a unit's last value (< 32 u16 values: poly_kword.cuh unpack_group_p);
+  // two per warp (TMA stores)
   a.capv = a.ut + 128u;
-  a.cap = (uint32_t)((a.capv * a.vb + 32 + 15) / 16 * 16);
+  a.cap = (uint32_t)((a.capv * a.vb + 32 + 64 + 15) / 16 * 16);
   a.o_warp = (uint32_t)((sizeof(d3::Ctl) + 127) / 128 * 128);
   a.o_ring = (a.o_warp + d3::NW * 2 * a.cap + 127) / 128 * 128;
   const uint32_t smax = 227 * 1024;

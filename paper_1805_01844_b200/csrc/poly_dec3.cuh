@@ -759,7 +759,6 @@ __global__ void __launch_bounds__(NTHR, 1) dec3_main(Args a) {
         if (nw_ok && k >= 4 && k <= 27 && k != 23 && k != 25 && k != 26) {
           fast = true;
           const uint32_t j1 = j0 + nwu, mtop = blen - (nw - 1) * k;
-          const uint32_t nfull = mtop < k ? nw - 1 : nw, jf = min(j1, nfull);
           const uint64_t gbase = gblk + (uint64_t)j0 * k * 2;  // 16-byte aligned (kw_ok, j0 % 8 == 0)
           uint8_t* blk = stg - 2ull * j0 * k;                 // block value 0 in staging coordinates
           const uint32_t lj = dc_log2b(dc);
@@ -770,24 +769,35 @@ __global__ void __launch_bounds__(NTHR, 1) dec3_main(Args a) {
   case KK: {                                                                                     \
     /* the group codec's power-of-two path is for B = 2^(64 / KK); the other \
        power-of-two bases of capacity KK (2^11 for 5, 2^13..2^15 for 4) go  \
-       word by word below */                                                \
+       word by word below.  The groups cover every word of the unit: an odd \
+       last word is paired with a zero word, and the block's short top word \
+       is decoded like a full one (checked against B^mtop below) */         \
     const uint32_t gb = j0 / kq<KK>();                                                           \
-    const uint32_t ge = (!p2 || lj == 64 / KK) ? jf / kq<KK>() : gb;                             \
-    if (ge > gb)                                                                                 \
-      err |= p2 ? unpack_groups_kp<KK, true>(PAY - j0, gb, ge, dc, B, h.y, blk)                  \
-                : unpack_groups_kp<KK, false>(PAY - j0, gb, ge, dc, B, h.y, blk);                \
-    jdone = max(j0, ge * kq<KK>());                                                              \
+    const uint32_t ge = (!p2 || lj == 64 / KK) ? (j1 + kq<KK>() - 1) / kq<KK>() : gb;            \
+    if (ge > gb) {                                                                               \
+      err |= p2 ? unpack_groups_kp<KK, true>(PAY - j0, gb, ge, j1, dc, B, h.y, blk)              \
+                : unpack_groups_kp<KK, false>(PAY - j0, gb, ge, j1, dc, B, h.y, blk);            \
+      jdone = j1;                                                                                \
+    }                                                                                            \
   } break;
             POLY_FOR_EACH_K16(POLY_D3K)
 #undef POLY_D3K
             default:
               break;
           }
-          for (uint32_t j = jdone + lane; j < j1; j += 32) {  // the odd word of a pair and / or the block's last word
-            const uint32_t m = (j + 1 == nw) ? mtop : k;
-            err |= dec_word_dc<V>(PAY[j - j0], dc, B, h.y, k, m, reinterpret_cast<V*>(stg) + (j - j0) * k);
+          if (jdone != j1) {
+            for (uint32_t j = jdone + lane; j < j1; j += 32) {  // capacities / bases without a group codec
+              const uint32_t m = (j + 1 == nw) ? mtop : k;
+              err |= dec_word_dc<V>(PAY[j - j0], dc, B, h.y, k, m, reinterpret_cast<V*>(stg) + (j - j0) * k);
+            }
           }
           __syncwarp();
+          // a9 for a short top word decoded by the group codec: s < B^mtop, i.e.
+          // its k - mtop digits past the block's end (staged as v_min + digit,
+          // never copied out) are 0
+          if (jdone == j1 && j1 == nw && (uint32_t)lane < k - mtop &&
+              reinterpret_cast<const V*>(blk)[blen + lane] != (V)h.y)
+            err |= POLY_ST_RESIDUE;
           const uint32_t nv = min(blen, j1 * k) - j0 * k;
           PROBE_ADD(2, cd0);
           PROBE_T0(cc0);

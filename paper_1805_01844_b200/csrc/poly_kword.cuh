@@ -322,45 +322,33 @@ __device__ __forceinline__ uint32_t unpack_regs_p(const uint64_t (&w)[KCls<K>::Q
   }
   return err;
 }
+// Group g of a block whose words [.., wend) are available: words at or past
+// wend (the second word of the block's last, odd pair) read as 0.  Every group
+// stores its Q K values, so the staging buffer holds up to K values past the
+// last real one (poly_dec3.cuh: the plan's slack).  A short top word is
+// decoded like a full one -- its digits past the block's end are not copied
+// out; the caller checks it against B^m.
 template <int K, bool POW2>
-__device__ __forceinline__ uint32_t unpack_group_p(const uint64_t* src, uint32_t g, const DecConst& dc, uint32_t B,
-                                                   uint32_t vmin, uint8_t* blk) {
+__device__ __forceinline__ uint32_t unpack_group_p(const uint64_t* src, uint32_t g, uint32_t wend, const DecConst& dc,
+                                                   uint32_t B, uint32_t vmin, uint8_t* blk) {
   using C = KCls<K>;
   uint64_t w[C::Q];
   uint32_t r[C::NR];
 #pragma unroll
-  for (int q = 0; q < C::Q; ++q) w[q] = src[g * C::Q + q];
+  for (int q = 0; q < C::Q; ++q) {
+    const uint32_t j = g * C::Q + q;
+    w[q] = (q == 0 || j < wend) ? src[j] : 0ull;
+  }
   const uint32_t err = unpack_regs_p<K, POW2>(w, dc, B, vmin, r);
   store_group<K>(blk + (size_t)g * C::BYTES, r);
   return err;
 }
-#ifndef POLY_KP_PAIR
-#define POLY_KP_PAIR 0
-#endif
+// Groups [gb, ge) of a block, lane-strided, by one warp; returns status bits.
 template <int K, bool POW2>
-__device__ __forceinline__ uint32_t unpack_groups_kp(const uint64_t* src, uint32_t gb, uint32_t ge, const DecConst& dc,
-                                                     uint32_t B, uint32_t vmin, uint8_t* blk) {
+__device__ __forceinline__ uint32_t unpack_groups_kp(const uint64_t* src, uint32_t gb, uint32_t ge, uint32_t wend,
+                                                     const DecConst& dc, uint32_t B, uint32_t vmin, uint8_t* blk) {
   uint32_t err = 0;
-  uint32_t g = gb + (threadIdx.x & 31);
-#if POLY_KP_PAIR
-  // two groups per lane per step (independent multiply chains), the second
-  // one clamped to a valid group and not stored when past the end
-  using C = KCls<K>;
-  for (; g + 32 < ge; g += 64) {
-    uint64_t w0[C::Q], w1[C::Q];
-    uint32_t r0[C::NR], r1[C::NR];
-#pragma unroll
-    for (int q = 0; q < C::Q; ++q) {
-      w0[q] = src[g * C::Q + q];
-      w1[q] = src[(g + 32) * C::Q + q];
-    }
-    err |= unpack_regs_p<K, POW2>(w0, dc, B, vmin, r0);
-    err |= unpack_regs_p<K, POW2>(w1, dc, B, vmin, r1);
-    store_group<K>(blk + (size_t)g * C::BYTES, r0);
-    store_group<K>(blk + (size_t)(g + 32) * C::BYTES, r1);
-  }
-#endif
-  for (; g < ge; g += 32) err |= unpack_group_p<K, POW2>(src, g, dc, B, vmin, blk);
+  for (uint32_t g = gb + (threadIdx.x & 31); g < ge; g += 32) err |= unpack_group_p<K, POW2>(src, g, wend, dc, B, vmin, blk);
   return err;
 }
 

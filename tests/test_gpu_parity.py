@@ -272,6 +272,34 @@ def test_corruption_status_bits(large):
     assert _status(s[:pay] + bad_word + s[pay + 8:], n, L) & pc.POLY_ST_RESIDUE
 
 
+@pytest.mark.parametrize("L,lo,hi", [(1024, 1800, 2130), (4096, 0, 40), (1000, 0, 16), (77, 100, 350)])
+def test_short_top_word_bound(L, lo, hi):
+    """A block's short top word holds m < k digits: the decoder must accept
+    B^m - 1 and report RESIDUE for B^m (< B^k, so only the digits past the
+    block's end tell), in the two-pass decoder's group codec (odd and even k,
+    a power-of-two base) and in its word-by-word path."""
+    rng = np.random.default_rng(L + hi)
+    nbl = 5
+    x = rng.integers(lo, hi, L * nbl).astype(np.uint16)
+    x[::L] = lo
+    x[1::L] = hi - 1
+    B = hi - lo
+    k = 1
+    while B ** (k + 1) <= 1 << 64:
+        k += 1
+    m = L % k
+    assert m != 0
+    nw = (L + k - 1) // k
+    s = _stream(x, L)
+    pay = 32 + 16 * nbl
+    for blk in (0, nbl - 1):
+        top = pay + 8 * (nw * blk + nw - 1)
+        ok_word = struct.pack("<Q", B ** m - 1)
+        bad_word = struct.pack("<Q", B ** m)
+        assert _status(s[:top] + ok_word + s[top + 8:], x.size, L) == 0
+        assert _status(s[:top] + bad_word + s[top + 8:], x.size, L) & pc.POLY_ST_RESIDUE
+
+
 def test_empty_input_rejected():
     x = torch.empty(0, dtype=torch.uint16, device="cuda")
     with pytest.raises(pc.PolyError) as e:
