@@ -1049,7 +1049,8 @@ poly_status_t poly_decompress(const void* d_in, uint64_t compressed_bytes, poly_
     d.cst_w = reinterpret_cast<uint64_t*>(ws + dp.o_cw);
     d.cst_u = reinterpret_cast<uint64_t*>(ws + dp.o_cu);
     d.T = reinterpret_cast<uint4*>(ws + dp.o_T);
-    d.kw_ok = (dt == POLY_U16 && (reinterpret_cast<uintptr_t>(d_out) & 15) == 0 && (sh.Le * 2) % 16 == 0) ? 1u : 0u;
+    d.kw_ok = dt != POLY_U16 ? 0u
+              : ((reinterpret_cast<uintptr_t>(d_out) & 15) == 0 && (sh.Le * 2) % 16 == 0) ? 1u : 2u;
     cudaMemsetAsync(ws, 0, dp.o_T, s);
     const uint64_t sms = (uint64_t)(g_sms[dev] > 0 ? g_sms[dev] : 148);
     const unsigned g1 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(d.n_chunks, 4 * sms));

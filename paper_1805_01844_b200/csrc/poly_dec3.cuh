@@ -72,7 +72,8 @@ struct Args {
   uint64_t n, Le, n_blocks, last_len, n_chunks, max_units;
   uint32_t block_len, width, vb, kmin_log2;
   uint32_t ut;           // values per unit (target)
-  uint32_t kw_ok;        // u16 blocks start 16-byte aligned in the output: k-specialised codec
+  uint32_t kw_ok;        // u16: k-specialised codec; 1 = blocks start 16-byte aligned in the output (TMA
+                         // stores), 2 = any alignment (staged values copied out by the warp)
   uint32_t capv;         // values a unit may hold (the staging buffer's capacity)
   uint32_t cap;          // bytes per staging buffer (two per warp)
   uint32_t o_warp, o_ring, ring_bytes;
@@ -372,6 +373,28 @@ __device__ __forceinline__ void store_out(const uint8_t* stg, uint64_t G0, uint6
     const uint32_t ne = (uint32_t)(c_hi - c_lo) / sizeof(V);
     if ((uint32_t)lane < ne) reinterpret_cast<V*>(c_lo)[lane] = reinterpret_cast<const V*>(stg + (c_lo - G0))[lane];
   }
+}
+
+// u16 values staged from a 16-byte aligned address to a global address of
+// any (2-byte) alignment: 4-byte stores, the pairs funnel-shifted when the
+// destination sits 2 bytes off, and single values at the ends.
+__device__ __forceinline__ void copy_out_u16(const uint8_t* stg, uint64_t gbase, uint32_t nv, int lane) {
+  if (nv == 0) return;
+  const uint16_t* s = reinterpret_cast<const uint16_t*>(stg);
+  uint16_t* g = reinterpret_cast<uint16_t*>(gbase);
+  const uint32_t head = (uint32_t)(gbase >> 1) & 1u;  // values before 4-byte alignment
+  const uint32_t np = (nv - head) >> 1;
+  uint32_t* G = reinterpret_cast<uint32_t*>(g + head);
+  const uint32_t* S = reinterpret_cast<const uint32_t*>(stg);
+  if (head == 0) {
+#pragma unroll 4
+    for (uint32_t i = lane; i < np; i += 32) G[i] = S[i];
+  } else {
+    if (lane == 0) g[0] = s[0];
+#pragma unroll 4
+    for (uint32_t i = lane; i < np; i += 32) G[i] = __funnelshift_r(S[i], S[i + 1], 16);
+  }
+  if (((nv - head) & 1u) && lane == 31) g[nv - 1] = s[nv - 1];
 }
 
 // Fill the global byte range [g_lo, g_hi) with the value v (CONSTANT block).
@@ -759,7 +782,7 @@ __global__ void __launch_bounds__(NTHR, 1) dec3_main(Args a) {
         if (nw_ok && k >= 4 && k <= 27 && k != 23 && k != 25 && k != 26) {
           fast = true;
           const uint32_t j1 = j0 + nwu, mtop = blen - (nw - 1) * k;
-          const uint64_t gbase = gblk + (uint64_t)j0 * k * 2;  // 16-byte aligned (kw_ok, j0 % 8 == 0)
+          const uint64_t gbase = gblk + (uint64_t)j0 * k * 2;  // kw_ok 1: 16-byte aligned (j0 % 8 == 0)
           uint8_t* blk = stg - 2ull * j0 * k;                 // block value 0 in staging coordinates
           const uint32_t lj = dc_log2b(dc);
           const bool p2 = lj != 0;
@@ -801,7 +824,10 @@ __global__ void __launch_bounds__(NTHR, 1) dec3_main(Args a) {
           const uint32_t nv = min(blen, j1 * k) - j0 * k;
           PROBE_ADD(2, cd0);
           PROBE_T0(cc0);
-          store_out<V>(stg, gbase, gbase, gbase + (uint64_t)nv * 2, lane);
+          if (a.kw_ok == 1)
+            store_out<V>(stg, gbase, gbase, gbase + (uint64_t)nv * 2, lane);
+          else
+            copy_out_u16(stg, gbase, nv, lane);
           PROBE_ADD(3, cc0);
         }
       }
