@@ -47,9 +47,15 @@ using d3::g_probe;
 constexpr int NW = POLY_C3_NW;           // consumer warps
 constexpr int NWR = POLY_C3_NWR;         // writer warps
 constexpr int NTHR = 32 * (NW + 1 + NWR);
-constexpr int MAXS3 = 8;                 // slots
+#ifndef POLY_C3_MAXS
+#define POLY_C3_MAXS 8
+#endif
+#ifndef POLY_C3_TILE
+#define POLY_C3_TILE 24576
+#endif
+constexpr int MAXS3 = POLY_C3_MAXS;      // slots
 constexpr uint32_t TBMAX = 256;          // blocks per tile
-constexpr uint32_t C3_TILE = 24576;      // value bytes per tile (target)
+constexpr uint32_t C3_TILE = POLY_C3_TILE;  // value bytes per tile (target)
 constexpr uint32_t C3_CLAIM = 8192;      // value bytes per consumer claim (target; small blocks)
 
 struct __align__(16) Ctl {
