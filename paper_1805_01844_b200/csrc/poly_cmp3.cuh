@@ -47,6 +47,9 @@ using d3::g_probe;
 constexpr int NW = POLY_C3_NW;           // consumer warps
 constexpr int NWR = POLY_C3_NWR;         // writer warps
 constexpr int NTHR = 32 * (NW + 1 + NWR);
+// slots and tile size (A/B knobs; measured, cfg5 / cfg4 compress GB/s against
+// 3545 / 2436: 16 KiB x 12 slots 2877 / 2278, 8 KiB x 24 1824 / 1551, 32 KiB x 6
+// with 3 writers 3575 / 2392, with 2 writers 3664 / 1990, 48 KiB x 4 3421 / 2026)
 #ifndef POLY_C3_MAXS
 #define POLY_C3_MAXS 8
 #endif
