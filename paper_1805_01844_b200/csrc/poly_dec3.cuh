@@ -376,25 +376,38 @@ __device__ __forceinline__ void store_out(const uint8_t* stg, uint64_t G0, uint6
 }
 
 // u16 values staged from a 16-byte aligned address to a global address of
-// any (2-byte) alignment: 4-byte stores, the pairs funnel-shifted when the
-// destination sits 2 bytes off, and single values at the ends.
+// any (2-byte) alignment: 8-byte stores of the 8-byte aligned interior, the
+// word pairs funnel-shifted when the destination sits an odd number of values
+// off a 4-byte boundary, and single values at the ends.
 __device__ __forceinline__ void copy_out_u16(const uint8_t* stg, uint64_t gbase, uint32_t nv, int lane) {
   if (nv == 0) return;
   const uint16_t* s = reinterpret_cast<const uint16_t*>(stg);
   uint16_t* g = reinterpret_cast<uint16_t*>(gbase);
-  const uint32_t head = (uint32_t)(gbase >> 1) & 1u;  // values before 4-byte alignment
-  const uint32_t np = (nv - head) >> 1;
-  uint32_t* G = reinterpret_cast<uint32_t*>(g + head);
-  const uint32_t* S = reinterpret_cast<const uint32_t*>(stg);
-  if (head == 0) {
-#pragma unroll 4
-    for (uint32_t i = lane; i < np; i += 32) G[i] = S[i];
-  } else {
-    if (lane == 0) g[0] = s[0];
-#pragma unroll 4
-    for (uint32_t i = lane; i < np; i += 32) G[i] = __funnelshift_r(S[i], S[i + 1], 16);
+  const uint64_t gend = gbase + 2ull * nv;
+  const uint64_t a8 = (gbase + 7) & ~7ull, b8 = gend & ~7ull;
+  if (a8 >= b8) {  // fewer than 8 values
+    if ((uint32_t)lane < nv) g[lane] = s[lane];
+    return;
   }
-  if (((nv - head) & 1u) && lane == 31) g[nv - 1] = s[nv - 1];
+  const uint32_t o = (uint32_t)(a8 - gbase);  // staging byte of the first aligned chunk: 0, 2, 4 or 6
+  const uint32_t nch = (uint32_t)((b8 - a8) >> 3);
+  const uint32_t* S = reinterpret_cast<const uint32_t*>(stg + (o & ~3u));
+  uint2* G = reinterpret_cast<uint2*>(a8);
+  if ((o & 2u) == 0) {
+#pragma unroll 4
+    for (uint32_t c = lane; c < nch; c += 32) G[c] = make_uint2(S[2 * c], S[2 * c + 1]);
+  } else {
+#pragma unroll 4
+    for (uint32_t c = lane; c < nch; c += 32) {
+      const uint32_t w0 = S[2 * c], w1 = S[2 * c + 1], w2 = S[2 * c + 2];
+      G[c] = make_uint2(__funnelshift_r(w0, w1, 16), __funnelshift_r(w1, w2, 16));
+    }
+  }
+  const uint32_t nh = o >> 1, nt = (uint32_t)(gend - b8) >> 1, t0 = (uint32_t)(b8 - gbase) >> 1;
+  if ((uint32_t)lane < nh)
+    g[lane] = s[lane];
+  else if ((uint32_t)lane < nh + nt)
+    g[t0 + lane - nh] = s[t0 + lane - nh];
 }
 
 // Fill the global byte range [g_lo, g_hi) with the value v (CONSTANT block).

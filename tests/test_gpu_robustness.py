@@ -173,3 +173,29 @@ def test_unaligned_value_arrays(oracle_lib, idx, shift):
     assert int(st.item()) == 0
     assert torch.equal(yv, xv)
     assert int(ybig[:shift].abs().sum().item()) == 0 and int(ybig[shift + n:].abs().sum().item()) == 0
+
+
+@pytest.mark.parametrize("L,n", [(77, 77 * 40 + 3), (1855, 1855 * 9 + 5), (1024, 1024 * 12 + 1), (4096, 4096 * 5 + 2049)])
+def test_u16_every_output_offset(oracle_lib, L, n):
+    """Two-pass decoder, u16: the output array starting 0..7 elements past a
+    16-byte boundary (aligned TMA stores, 8-byte copy-out with and without the
+    funnel shift, its head / tail values, units of fewer than 8 values), block
+    lengths that are and are not a multiple of 16 bytes, a short last block;
+    nothing is written outside the array."""
+    rng = np.random.default_rng(L + n)
+    x = rng.integers(900, 1230, n).astype(np.uint16)
+    x[L:2 * L] = rng.integers(0, 16, L).astype(np.uint16)        # a power-of-two base
+    x[2 * L:3 * L] = rng.integers(10, 51, L).astype(np.uint16)   # another capacity
+    ref = oracle_lib.compress(x, L)
+    xd = to_dev(x)
+    out, nb = pc.poly_compress(xd, L)
+    nbytes = int(nb.item())
+    assert out[:nbytes].cpu().numpy().tobytes() == ref
+    for shift in range(8):
+        ybig = torch.zeros(n + 16, dtype=torch.int16, device="cuda")
+        yv = ybig[shift:shift + n].view(torch.uint16)
+        _, st = pc.poly_decompress(out, nbytes, 16, n, L, out=yv)
+        torch.cuda.synchronize()
+        assert int(st.item()) == 0, shift
+        assert torch.equal(yv, xd), shift
+        assert int(ybig[:shift].abs().sum().item()) == 0 and int(ybig[shift + n:].abs().sum().item()) == 0, shift
