@@ -144,6 +144,43 @@ __device__ __forceinline__ void pack_group(const uint8_t* blk, uint32_t g, const
   }
 }
 
+// The same for a block that starts at any 2-byte aligned address (block
+// lengths that are not a multiple of 16 bytes): the values are read one by
+// one, 16 bits each, along the Horner chains.
+template <int K>
+__device__ __forceinline__ void pack_group_u(const uint16_t* blk, uint32_t g, const KPack& c, uint64_t* dst) {
+  using C = KCls<K>;
+  const uint16_t* v = blk + (size_t)g * C::VALS;
+#pragma unroll
+  for (int q = 0; q < C::Q; ++q) {
+    const int o = q * K;
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int i = C::H0 - 1; i >= 0; --i) lo = lo * c.B + v[o + i];
+#pragma unroll
+    for (int i = 2 * C::H0 - 1; i >= C::H0; --i) hi = hi * c.B + v[o + i];
+    lo -= c.corr;
+    hi -= c.corr;
+    uint64_t s;
+    if (K & 1) {
+      const uint32_t top = (uint32_t)v[o + K - 1] - c.vmin;
+      s = ((uint64_t)top * c.D + hi) * c.D + lo;
+    } else {
+      s = (uint64_t)hi * c.D + lo;
+    }
+    dst[g * C::Q + q] = s;
+  }
+}
+template <int K>
+__device__ __forceinline__ uint32_t pack_block_ku(const uint16_t* blk, uint32_t nb, uint32_t B, uint32_t vmin,
+                                                  uint32_t g0, uint32_t gstep, uint64_t* dst) {
+  using C = KCls<K>;
+  const uint32_t ngroups = nb / C::VALS;
+  const KPack c = kpack_consts<K>(B, vmin);
+  for (uint32_t g = g0; g < ngroups; g += gstep) pack_group_u<K>(blk, g, c, dst);
+  return ngroups * C::Q;
+}
+
 // Unpack group g of a block (all Q words full).  Returns POLY_ST_RESIDUE if a
 // word is >= B^K.
 template <int K>

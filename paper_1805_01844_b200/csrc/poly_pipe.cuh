@@ -1088,6 +1088,19 @@ __global__ void __launch_bounds__(NW * 32 + 32 * (2 + NLB_MAX), POLY_CTAS) poly_
             default:
               break;
           }
+        } else if (sizeof(V) == 2) {
+          // blocks at any 2-byte alignment: the same chains over 16-bit reads
+          const uint16_t* blk = reinterpret_cast<const uint16_t*>(src);
+          switch (k) {
+#define POLY_PKU(KK)                                                                             \
+  case KK:                                                                                       \
+    done = pack_block_ku<KK>(blk, nb, (uint32_t)B, vm, part * 32 + lane, 32 * G, dst);           \
+    break;
+            POLY_FOR_EACH_K16(POLY_PKU)
+#undef POLY_PKU
+            default:
+              break;
+          }
         }
         for (uint32_t j = done + part * 32 + lane; j < nwk; j += 32 * G) {
           const uint32_t first = j * k;
